@@ -1,0 +1,132 @@
+"""Host-side plumbing: the reference's batch conventions over device tensors.
+
+Mirrors /root/reference/pkg/src/batchfact/core.py:
+  * ``BatchError(index, cause)`` -- lowest failing entry (core.py:17-23, :120-122);
+  * ``as_matrix`` -- 2-d check, non-f32/f64 cast to f64, column-major (core.py:26-33).
+The reference's ``batch_apply`` (core.py:97-123) runs one Python call per entry; here a
+homogeneous group of entries becomes ONE C-ABI call. Torch is used only for device
+memory, streams and copies (pinned host staging); no compute happens in torch.
+"""
+
+import numpy as np
+import torch
+
+from . import _lib
+
+REAL_DTYPES = (np.float32, np.float64)
+
+
+class BatchError(Exception):
+    """Failure of a per-entry operation inside a batch, tagged with the index."""
+
+    def __init__(self, index, cause):
+        super().__init__(f"batch entry {index}: {cause}")
+        self.index = index
+        self.cause = cause
+
+
+def as_matrix(a, dtype=None):
+    """Coerce ``a`` to a 2-d column-major float array (core.py:26-33)."""
+    a = np.asarray(a, dtype=dtype)
+    if a.ndim != 2:
+        raise ValueError(f"expected a 2-d array, got ndim={a.ndim}")
+    if a.dtype.type not in REAL_DTYPES:
+        a = a.astype(np.float64)
+    return np.asfortranarray(a)
+
+
+def resolve_device(device=None):
+    if not torch.cuda.is_available():
+        raise _lib.BackendUnavailable("no CUDA device visible; batchfact_b200 has no CPU fallback")
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    device = torch.device(device)
+    if device.type != "cuda":
+        raise ValueError("batchfact_b200 runs on CUDA devices only")
+    if device.index is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    return device
+
+
+def stream_handle(device):
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def workspace(nbytes, device):
+    if nbytes == 0:
+        return None, 0
+    return torch.empty(int(nbytes), dtype=torch.uint8, device=device), int(nbytes)
+
+
+def colmajor(t):
+    """(B, m, n) tensor -> (B, n, m) contiguous storage == per-matrix column-major."""
+    return t.transpose(-1, -2).contiguous()
+
+
+def from_colmajor(store):
+    """(B, cols, rows) contiguous storage -> (B, rows, cols) view (column-major strides)."""
+    return store.transpose(-1, -2)
+
+
+def torch_dtype(np_dtype):
+    return torch.float64 if np.dtype(np_dtype) == np.float64 else torch.float32
+
+
+def check_batched_tensor(a, what):
+    if not isinstance(a, torch.Tensor):
+        raise TypeError(f"{what}: expected a torch.Tensor")
+    if a.dim() != 3:
+        raise ValueError(f"{what}: expected a (batch, m, n) tensor, got shape {tuple(a.shape)}")
+    if a.dtype not in (torch.float32, torch.float64):
+        raise ValueError(f"{what}: dtype must be float32 or float64")
+    if a.device.type != "cuda":
+        raise ValueError(f"{what}: tensor must live on a CUDA device")
+
+
+def group_entries(entries, validate):
+    """Coerce entries, validate each (reference error semantics), group by (shape, dtype).
+
+    Returns {(m, n, dtype): [indices]} and the coerced list. Raises BatchError for the
+    lowest failing index before any launch (the reference raises it after running the
+    batch, with identical outcome, core.py:104-123).
+    """
+    mats = []
+    errors = {}
+    for i, e in enumerate(entries):
+        try:
+            a = as_matrix(e)
+            validate(a)
+            mats.append(a)
+        except Exception as exc:  # noqa: BLE001 - reported with the batch index
+            errors[i] = exc
+            mats.append(None)
+    if errors:
+        i = min(errors)
+        raise BatchError(i, errors[i]) from errors[i]
+    groups = {}
+    for i, a in enumerate(mats):
+        groups.setdefault((a.shape[0], a.shape[1], a.dtype.str), []).append(i)
+    return groups, mats
+
+
+def stack_to_device(mats, idx, device):
+    """Stack entries (Fortran arrays) into pinned host memory, copy to device: (G, n, m)."""
+    first = mats[idx[0]]
+    m, n = first.shape
+    host = torch.empty((len(idx), n, m), dtype=torch_dtype(first.dtype), pin_memory=True)
+    hv = host.numpy()
+    for j, i in enumerate(idx):
+        hv[j] = mats[i].T
+    return host.to(device, non_blocking=True)
+
+
+def to_host(t):
+    """Device tensor -> numpy (synchronising copy through pinned memory)."""
+    host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    host.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return host.numpy()

@@ -1,0 +1,396 @@
+// C ABI (include/batchfact_b200.h): validation, workspace planning, dispatch.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "../../include/batchfact_b200.h"
+#include "internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, int a = 0, int b = 0, int c = 0) {
+  char buf[512];
+  snprintf(buf, sizeof(buf), fmt, a, b, c);
+  g_err = buf;
+  return code;
+}
+
+int cuda_rc(int rc, const char* where) {
+  if (rc == 0) return BF_OK;
+  char buf[512];
+  snprintf(buf, sizeof(buf), "%s: CUDA error %d (%s)", where, rc, cudaGetErrorString((cudaError_t)rc));
+  g_err = buf;
+  return rc;
+}
+
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+int check_ws(void* ws, size_t have, size_t need) {
+  if (need == 0) return BF_OK;
+  if (!ws || have < need) {
+    char buf[256];
+    snprintf(buf, sizeof(buf), "workspace too small: need %zu bytes, got %zu", need, ws ? have : (size_t)0);
+    g_err = buf;
+    return BF_ERR_WORKSPACE;
+  }
+  return BF_OK;
+}
+
+// ---------------------------------------------------------------- QR
+template <typename T>
+int qr_impl(int64_t batch, int m, int n, const T* a, T* q, T* r, int pw, void* ws, size_t wsb, void* st) {
+  if (batch < 0 || m < 0 || n < 0) return fail(BF_ERR_ARG, "negative batch or shape");
+  // qr.py:71-74
+  if (m < n) return fail(BF_ERR_ARG, "qr requires m >= n, got %d x %d; pass the transpose", m, n);
+  if (pw < 1) return fail(BF_ERR_ARG, "panel_width must be >= 1");
+  int dt = sizeof(T) == 8 ? 0 : 1;
+  int rc = check_ws(ws, wsb, bf::qr_global_ws_bytes(dt, batch, m, n));
+  if (rc) return rc;
+  return cuda_rc(bf::launch_qr(dt, batch, m, n, a, (int64_t)m * n, q, (int64_t)m * n, r, (int64_t)n * n, ws, S(st)),
+                 "qr");
+}
+
+// ---------------------------------------------------------------- SVD
+double resolve_tol(double t, bool f64, bool block) {
+  if (t > 0) return t;
+  if (block) return f64 ? bf::Tol<double>::block : bf::Tol<float>::block;
+  return f64 ? bf::Tol<double>::svd : bf::Tol<float>::svd;
+}
+
+int check_jopts(const bf_jacobi_opts* o) {
+  if (!o) return fail(BF_ERR_ARG, "opts is NULL");
+  if (o->max_sweeps < 1) return fail(BF_ERR_ARG, "max_sweeps must be >= 1");
+  if (o->ordering != 0 && o->ordering != 1) return fail(BF_ERR_ARG, "ordering must be one of ('serial', 'round_robin')");
+  if (o->tier < 0 || o->tier > 2) return fail(BF_ERR_ARG, "tier must be 0 (auto), 1 (register) or 2 (shared)");
+  if (!(o->tolerance == o->tolerance)) return fail(BF_ERR_ARG, "tolerance must be positive");
+  return BF_OK;
+}
+
+template <typename T>
+int svd_impl(int64_t batch, int m, int n, const T* a, T* u, T* s, T* v, int32_t* sweeps, uint8_t* conv, int64_t* rots,
+             const bf_jacobi_opts* o, void* ws, size_t wsb, void* st) {
+  int rc = check_jopts(o);
+  if (rc) return rc;
+  if (batch < 0 || m < 0 || n < 0) return fail(BF_ERR_ARG, "negative batch or shape");
+  if (m < n) return fail(BF_ERR_ARG, "svd requires m >= n, got %d x %d; pass the transpose", m, n);
+  if (o->accumulate_v && !v) return fail(BF_ERR_ARG, "accumulate_v set but v is NULL");
+  const bool f64 = sizeof(T) == 8;
+  int dt = f64 ? 0 : 1;
+  if (n == 0) {  // jacobi.py:244-249: empty result, converged, 0 sweeps
+    if (batch > 0) {
+      if (sweeps) cudaMemsetAsync(sweeps, 0, sizeof(int32_t) * batch, S(st));
+      if (conv) cudaMemsetAsync(conv, 1, batch, S(st));
+      if (rots) cudaMemsetAsync(rots, 0, sizeof(int64_t) * batch, S(st));
+    }
+    return cuda_rc((int)cudaGetLastError(), "svd");
+  }
+  rc = check_ws(ws, wsb, bf::svd_global_ws_bytes(dt, batch, m, n, o->ordering, o->accumulate_v != 0, o->tier));
+  if (rc) return rc;
+  bf::SvdLaunch L;
+  L.batch = batch;
+  L.m = m;
+  L.n = n;
+  L.a = a;
+  L.a_stride = (int64_t)m * n;
+  L.u = u;
+  L.u_stride = (int64_t)m * n;
+  L.s = s;
+  L.s_stride = n;
+  L.v = o->accumulate_v ? v : nullptr;
+  L.v_stride = (int64_t)n * n;
+  L.sweeps = sweeps;
+  L.converged = conv;
+  L.rotations = rots;
+  L.tol = resolve_tol(o->tolerance, f64, false);
+  L.max_sweeps = o->max_sweeps;
+  L.ordering = o->ordering;
+  L.tier = o->tier;
+  L.transpose_a = false;
+  return cuda_rc(bf::launch_svd(dt, L, ws, S(st)), "svd");
+}
+
+// ---------------------------------------------------------------- block SVD
+int check_bopts(const bf_block_opts* o) {
+  if (!o) return fail(BF_ERR_ARG, "opts is NULL");
+  if (o->block_width < 1) return fail(BF_ERR_ARG, "block_width must be >= 1");
+  if (o->method != 0 && o->method != 1) return fail(BF_ERR_ARG, "method must be one of ('gram', 'direct')");
+  if (o->max_sweeps < 1) return fail(BF_ERR_ARG, "max_sweeps must be >= 1");
+  return BF_OK;
+}
+
+template <typename T>
+int block_impl(int64_t batch, int m, int n, const T* a, T* u, T* s, T* v, int32_t* sweeps, uint8_t* conv, T* eh,
+               const bf_block_opts* o, void* ws, size_t wsb, void* st) {
+  int rc = check_bopts(o);
+  if (rc) return rc;
+  if (batch < 0 || m < 0 || n < 0) return fail(BF_ERR_ARG, "negative batch or shape");
+  if (m < n) return fail(BF_ERR_ARG, "block_svd requires m >= n, got %d x %d", m, n);
+  if (o->accumulate_v && !v) return fail(BF_ERR_ARG, "accumulate_v set but v is NULL");
+  if (!sweeps || !conv) return fail(BF_ERR_ARG, "sweeps and converged are required for block_svd");
+  int k = o->block_width;
+  if (o->method == 1) k = std::max(1, std::min(k, m / 2));
+  if (2 * k > 64) return fail(BF_ERR_UNSUPPORTED, "block_width %d unsupported (2*block_width must be <= 64)", k);
+  if (m == 0) return fail(BF_ERR_UNSUPPORTED, "block_svd of an empty matrix is unsupported");
+  const bool f64 = sizeof(T) == 8;
+  int dt = f64 ? 0 : 1;
+  rc = check_ws(ws, wsb, bf::block_ws_bytes(dt, batch, m, n, o->block_width, o->method, o->accumulate_v != 0));
+  if (rc) return rc;
+  bf::BlockLaunch L;
+  L.batch = batch;
+  L.m = m;
+  L.n = n;
+  L.a = a;
+  L.u = u;
+  L.s = s;
+  L.v = o->accumulate_v ? v : nullptr;
+  L.sweeps = sweeps;
+  L.converged = conv;
+  L.e_history = eh;
+  L.block_width = o->block_width;
+  L.method = o->method;
+  L.max_sweeps = o->max_sweeps;
+  L.tol = resolve_tol(o->tolerance, f64, true);
+  return cuda_rc(bf::launch_block_svd(dt, L, ws, S(st)), "block_svd");
+}
+
+// ---------------------------------------------------------------- rsvd
+struct RsvdLayout {
+  size_t omega, y, q, r, bt, qb, rb, ur, vr, svdws, total;
+};
+
+RsvdLayout rsvd_layout(int64_t batch, int m, int n, int w, int es, bool need_omega) {
+  RsvdLayout L;
+  size_t off = 0;
+  auto take = [&](size_t elems) {
+    size_t o = off;
+    off += al(elems * es);
+    return o;
+  };
+  L.omega = need_omega ? take((size_t)batch * n * w) : 0;
+  L.y = take((size_t)batch * m * w);
+  L.q = take((size_t)batch * m * w);
+  L.r = take((size_t)batch * w * w);
+  L.bt = take((size_t)batch * n * w);
+  L.qb = take((size_t)batch * n * w);
+  L.rb = take((size_t)batch * w * w);
+  L.ur = take((size_t)batch * w * w);
+  L.vr = take((size_t)batch * w * w);
+  size_t qws = std::max(bf::qr_global_ws_bytes(es == 8 ? 0 : 1, batch, m, w),
+                        bf::qr_global_ws_bytes(es == 8 ? 0 : 1, batch, n, w));
+  size_t sws = bf::svd_global_ws_bytes(es == 8 ? 0 : 1, batch, w, w, 1, true, 0);
+  L.svdws = off;
+  off += al(std::max(qws, sws));
+  L.total = off;
+  return L;
+}
+
+template <typename T>
+int rsvd_impl(int64_t batch, int m, int n, int k, int p, uint64_t slo, uint64_t shi, int64_t ibase, const T* a,
+              const T* omega, T* u, T* s, T* v, void* ws, size_t wsb, void* st) {
+  if (batch < 0 || m < 0 || n < 0) return fail(BF_ERR_ARG, "negative batch or shape");
+  if (k < 1) return fail(BF_ERR_ARG, "k must be >= 1");
+  if (p < 0) return fail(BF_ERR_ARG, "p must be >= 0");
+  const int w = k + p;
+  if (w > std::min(m, n))  // rsvd.py:60-64
+    return fail(BF_ERR_ARG, "k + p = %d exceeds min(m, n) = %d for shape (%d, ...)", w, std::min(m, n), m);
+  const bool f64 = sizeof(T) == 8;
+  if (!omega && !f64)
+    return fail(BF_ERR_UNSUPPORTED, "float32 rsvd needs a caller-supplied omega (device float ziggurat not built)");
+  const int es = sizeof(T), dt = f64 ? 0 : 1;
+  RsvdLayout Ly = rsvd_layout(batch, m, n, w, es, omega == nullptr);
+  int rc = check_ws(ws, wsb, Ly.total);
+  if (rc) return rc;
+  if (batch == 0) return BF_OK;
+  char* base = (char*)ws;
+  cudaStream_t cs = S(st);
+  T* om = omega ? (T*)omega : (T*)(base + Ly.omega);
+  T* Y = (T*)(base + Ly.y);
+  T* Q = (T*)(base + Ly.q);
+  T* R = (T*)(base + Ly.r);
+  T* Bt = (T*)(base + Ly.bt);
+  T* Qb = (T*)(base + Ly.qb);
+  T* Rb = (T*)(base + Ly.rb);
+  T* Ur = (T*)(base + Ly.ur);
+  T* Vr = (T*)(base + Ly.vr);
+  void* sws = base + Ly.svdws;
+  if (!omega) {  // gaussian_matrix(n, w, seed ^ i) (rsvd.py:65, :82-85)
+    rc = bf::launch_gaussian_f64(batch, n, w, slo, shi, ibase, 0, 0, (double*)om, (int64_t)n * w, cs);
+    if (rc) return cuda_rc(rc, "rsvd/omega");
+  }
+  bf::GemmLaunch g;
+  // Y = A @ Omega (rsvd.py:66)
+  g = bf::GemmLaunch{batch, m, w, n, a, m, (int64_t)m * n, false, om, n, (int64_t)n * w, false, Y, m, (int64_t)m * w};
+  if ((rc = bf::launch_gemm(dt, g, cs))) return cuda_rc(rc, "rsvd/gemm1");
+  // Q = qr(Y).q (rsvd.py:67)
+  if ((rc = bf::launch_qr(dt, batch, m, w, Y, (int64_t)m * w, Q, (int64_t)m * w, R, (int64_t)w * w, sws, cs)))
+    return cuda_rc(rc, "rsvd/qr1");
+  // B^T = A^T Q (n x w)  (B = Q^T A, rsvd.py:68)
+  g = bf::GemmLaunch{batch, n, w, m, a, m, (int64_t)m * n, true, Q, m, (int64_t)m * w, false, Bt, n, (int64_t)n * w};
+  if ((rc = bf::launch_gemm(dt, g, cs))) return cuda_rc(rc, "rsvd/gemm2");
+  // (Q_B, R_B) = qr(B^T) (rsvd.py:69)
+  if ((rc = bf::launch_qr(dt, batch, n, w, Bt, (int64_t)n * w, Qb, (int64_t)n * w, Rb, (int64_t)w * w, sws, cs)))
+    return cuda_rc(rc, "rsvd/qr2");
+  // svd(R_B^T, round_robin, accumulate_v) (rsvd.py:70-73)
+  bf::SvdLaunch L;
+  L.batch = batch;
+  L.m = w;
+  L.n = w;
+  L.a = Rb;
+  L.a_stride = (int64_t)w * w;
+  L.u = Ur;
+  L.u_stride = (int64_t)w * w;
+  L.s = s;
+  L.s_stride = w;
+  L.v = Vr;
+  L.v_stride = (int64_t)w * w;
+  L.sweeps = nullptr;
+  L.converged = nullptr;
+  L.rotations = nullptr;
+  L.tol = resolve_tol(0.0, f64, false);
+  L.max_sweeps = 30;
+  L.ordering = 1;
+  L.tier = 0;
+  L.transpose_a = true;
+  if ((rc = bf::launch_svd(dt, L, sws, cs))) return cuda_rc(rc, "rsvd/svd");
+  // U = Q @ U_R, V = Q_B @ V_R (rsvd.py:74-75)
+  g = bf::GemmLaunch{batch, m, w, w, Q, m, (int64_t)m * w, false, Ur, w, (int64_t)w * w, false, u, m, (int64_t)m * w};
+  if ((rc = bf::launch_gemm(dt, g, cs))) return cuda_rc(rc, "rsvd/gemm3");
+  g = bf::GemmLaunch{batch, n, w, w, Qb, n, (int64_t)n * w, false, Vr, w, (int64_t)w * w, false, v, n, (int64_t)n * w};
+  if ((rc = bf::launch_gemm(dt, g, cs))) return cuda_rc(rc, "rsvd/gemm4");
+  return BF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* bf_last_error(void) { return g_err.c_str(); }
+const char* bf_version(void) { return "batchfact_b200 0.1.0 (sm_100a)"; }
+
+size_t bf_qr_workspace_size(int64_t batch, int32_t m, int32_t n, int32_t es) {
+  if (m < n || m <= 0 || n <= 0) return 0;
+  return bf::qr_global_ws_bytes(es == 8 ? 0 : 1, batch, m, n);
+}
+int bf_qr_batched_f64(int64_t batch, int32_t m, int32_t n, const double* a, double* q, double* r, int32_t pw,
+                      void* ws, size_t wsb, void* st) {
+  return qr_impl<double>(batch, m, n, a, q, r, pw, ws, wsb, st);
+}
+int bf_qr_batched_f32(int64_t batch, int32_t m, int32_t n, const float* a, float* q, float* r, int32_t pw, void* ws,
+                      size_t wsb, void* st) {
+  return qr_impl<float>(batch, m, n, a, q, r, pw, ws, wsb, st);
+}
+
+size_t bf_svd_workspace_size(int64_t batch, int32_t m, int32_t n, int32_t es, const bf_jacobi_opts* o) {
+  if (!o || m < n || n <= 0) return 0;
+  return bf::svd_global_ws_bytes(es == 8 ? 0 : 1, batch, m, n, o->ordering, o->accumulate_v != 0, o->tier);
+}
+int bf_svd_batched_f64(int64_t batch, int32_t m, int32_t n, const double* a, double* u, double* s, double* v,
+                       int32_t* sweeps, uint8_t* conv, int64_t* rots, const bf_jacobi_opts* o, void* ws, size_t wsb,
+                       void* st) {
+  return svd_impl<double>(batch, m, n, a, u, s, v, sweeps, conv, rots, o, ws, wsb, st);
+}
+int bf_svd_batched_f32(int64_t batch, int32_t m, int32_t n, const float* a, float* u, float* s, float* v,
+                       int32_t* sweeps, uint8_t* conv, int64_t* rots, const bf_jacobi_opts* o, void* ws, size_t wsb,
+                       void* st) {
+  return svd_impl<float>(batch, m, n, a, u, s, v, sweeps, conv, rots, o, ws, wsb, st);
+}
+
+size_t bf_block_svd_workspace_size(int64_t batch, int32_t m, int32_t n, int32_t es, const bf_block_opts* o) {
+  if (!o || m < n || m <= 0 || o->block_width < 1) return 0;
+  return bf::block_ws_bytes(es == 8 ? 0 : 1, batch, m, n, o->block_width, o->method, o->accumulate_v != 0);
+}
+int bf_block_svd_batched_f64(int64_t batch, int32_t m, int32_t n, const double* a, double* u, double* s, double* v,
+                             int32_t* sweeps, uint8_t* conv, double* eh, const bf_block_opts* o, void* ws, size_t wsb,
+                             void* st) {
+  return block_impl<double>(batch, m, n, a, u, s, v, sweeps, conv, eh, o, ws, wsb, st);
+}
+int bf_block_svd_batched_f32(int64_t batch, int32_t m, int32_t n, const float* a, float* u, float* s, float* v,
+                             int32_t* sweeps, uint8_t* conv, float* eh, const bf_block_opts* o, void* ws, size_t wsb,
+                             void* st) {
+  return block_impl<float>(batch, m, n, a, u, s, v, sweeps, conv, eh, o, ws, wsb, st);
+}
+
+size_t bf_rsvd_workspace_size(int64_t batch, int32_t m, int32_t n, int32_t k, int32_t p, int32_t es) {
+  if (k < 1 || p < 0 || k + p > std::min(m, n)) return 0;
+  return rsvd_layout(batch, m, n, k + p, es, true).total;
+}
+int bf_rsvd_batched_f64(int64_t batch, int32_t m, int32_t n, int32_t k, int32_t p, uint64_t slo, uint64_t shi,
+                        int64_t ibase, const double* a, const double* omega, double* u, double* s, double* v, void* ws,
+                        size_t wsb, void* st) {
+  return rsvd_impl<double>(batch, m, n, k, p, slo, shi, ibase, a, omega, u, s, v, ws, wsb, st);
+}
+int bf_rsvd_batched_f32(int64_t batch, int32_t m, int32_t n, int32_t k, int32_t p, uint64_t slo, uint64_t shi,
+                        int64_t ibase, const float* a, const float* omega, float* u, float* s, float* v, void* ws,
+                        size_t wsb, void* st) {
+  return rsvd_impl<float>(batch, m, n, k, p, slo, shi, ibase, a, omega, u, s, v, ws, wsb, st);
+}
+
+int bf_gaussian_batched_f64(int64_t batch, int32_t rows, int32_t cols, uint64_t slo, uint64_t shi, int64_t ibase,
+                            int32_t mode, double* out, void* st) {
+  if (batch < 0 || rows < 0 || cols < 0) return fail(BF_ERR_ARG, "rows and cols must be >= 0");
+  return cuda_rc(bf::launch_gaussian_f64(batch, rows, cols, slo, shi, ibase, mode, 0, out, (int64_t)rows * cols, S(st)),
+                 "gaussian");
+}
+
+size_t bf_make_matrix_workspace_size(int64_t batch, int32_t m, int32_t n) {
+  return al((size_t)batch * m * n * 8) * 2 + al((size_t)batch * n * n * 8) * 3 + al((size_t)n * 8) +
+         std::max(bf::qr_global_ws_bytes(0, batch, m, n), bf::qr_global_ws_bytes(0, batch, n, n));
+}
+
+int bf_make_matrix_batched_f64(int64_t batch, int32_t m, int32_t n, int32_t mode, double cond, int32_t rank,
+                               uint64_t slo, uint64_t shi, int64_t ibase, double* a, double* sigma, void* ws,
+                               size_t wsb, void* st) {
+  if (m < n || n < 1) return fail(BF_ERR_ARG, "make_matrix requires m >= spec.n >= 1");
+  if (rank < 1 || rank > n) return fail(BF_ERR_ARG, "rank must be in [1, n]");
+  if (!(cond >= 1.0)) return fail(BF_ERR_ARG, "cond must be >= 1");
+  int rc = check_ws(ws, wsb, bf_make_matrix_workspace_size(batch, m, n));
+  if (rc) return rc;
+  if (batch == 0) return BF_OK;
+  cudaStream_t cs = S(st);
+  char* base = (char*)ws;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* p = base + off;
+    off += al(bytes);
+    return (double*)p;
+  };
+  double* G1 = take((size_t)batch * m * n * 8);
+  double* P = take((size_t)batch * m * n * 8);
+  double* G2 = take((size_t)batch * n * n * 8);
+  double* Qn = take((size_t)batch * n * n * 8);
+  double* Rr = take((size_t)batch * n * n * 8);
+  double* sg = take((size_t)n * 8);
+  void* qws = base + off;
+  // spectrum (testmat.py:51-65), same for every entry: computed on the host like numpy does
+  std::vector<double> h(n, 0.0);
+  if (rank == 1)
+    h[0] = 1.0;
+  else
+    for (int i = 0; i < rank; ++i)
+      h[i] = mode == 0 ? std::pow(cond, -(double)i / (double)(rank - 1))
+                       : 1.0 - (1.0 - 1.0 / cond) * (double)i / (double)(rank - 1);
+  if ((rc = (int)cudaMemcpyAsync(sg, h.data(), n * 8, cudaMemcpyHostToDevice, cs))) return cuda_rc(rc, "make_matrix");
+  if ((rc = (int)cudaMemcpyAsync(sigma, sg, n * 8, cudaMemcpyDeviceToDevice, cs))) return cuda_rc(rc, "make_matrix");
+  // P = random_orthonormal(m, n, seed), Q = random_orthonormal(n, n, seed ^ MIX) (testmat.py:68-80)
+  if ((rc = bf::launch_gaussian_f64(batch, m, n, slo, shi, ibase, 1, 0, G1, (int64_t)m * n, cs)))
+    return cuda_rc(rc, "make_matrix");
+  if ((rc = bf::launch_gaussian_f64(batch, n, n, slo, shi, ibase, 1, 0x9E3779B97F4A7C15ULL, G2, (int64_t)n * n, cs)))
+    return cuda_rc(rc, "make_matrix");
+  if ((rc = bf::launch_qr(0, batch, m, n, G1, (int64_t)m * n, P, (int64_t)m * n, Rr, (int64_t)n * n, qws, cs)))
+    return cuda_rc(rc, "make_matrix");
+  if ((rc = bf::launch_sign_fix_f64(batch, m, n, P, Rr, cs))) return cuda_rc(rc, "make_matrix");
+  if ((rc = bf::launch_qr(0, batch, n, n, G2, (int64_t)n * n, Qn, (int64_t)n * n, Rr, (int64_t)n * n, qws, cs)))
+    return cuda_rc(rc, "make_matrix");
+  if ((rc = bf::launch_sign_fix_f64(batch, n, n, Qn, Rr, cs))) return cuda_rc(rc, "make_matrix");
+  if ((rc = bf::launch_scale_cols_f64(batch, m, n, P, sg, cs))) return cuda_rc(rc, "make_matrix");
+  bf::GemmLaunch g{batch, m, n, n, P, m, (int64_t)m * n, false, Qn, n, (int64_t)n * n, true, a, m, (int64_t)m * n};
+  return cuda_rc(bf::launch_gemm(0, g, cs), "make_matrix");
+}
+
+}  // extern "C"

@@ -1,0 +1,406 @@
+// Batched one-sided block Jacobi SVD: global-memory tier.
+//
+// Reference: block_svd blockjacobi.py:84-168, batch_block_svd :171-174.
+// W (m x n_pad) and V (n_pad x n_pad) live in a global (L2-resident) workspace.
+// Each round-robin step over the n_blocks block columns is one kernel launch with
+// one CTA per (matrix, block pair); pairs of a step are disjoint, so running them
+// concurrently is exactly the reference's serial order (blockjacobi.py:110-111,120).
+//   gram  : G = pair^T pair (syrk, core.py:68-78), e = scaled_offdiag(G); if e > tol the
+//           inner round-robin SVD of G (no V) gives the rotation U_G; pair <- pair U_G with
+//           exactly-null directions zeroed (blockjacobi.py:124-134).
+//   direct: QR of the pair, e = scaled_offdiag(R); inner SVD of R with V; pair <-
+//           Q U_R diag(sigma) (applied as H_0..H_{2k-1} [U_R diag(sigma); 0]), rotation V_R
+//           (blockjacobi.py:135-143).
+// A per-sweep finalize kernel records e_history, counts the sweep and retires converged
+// matrices (blockjacobi.py:150-154); converged matrices simply stop (per-matrix, :171-174).
+#include "internal.h"
+#include "jacobi_cta.cuh"
+#include "qr_cta.cuh"
+
+namespace bf {
+
+template <typename T>
+struct BJArgs {
+  int64_t batch;
+  int m, n, n_pad, k, nb;  // k = block width, nb = n_pad / k
+  T* W;                    // batch x m x n_pad
+  T* V;                    // batch x n_pad x n_pad or null
+  T* P;                    // direct method: per-CTA pair scratch (batch*nb/2 x m x 2k) when not in smem
+  double* e_sweep;         // batch
+  uint8_t* active;         // batch
+  int32_t* sweeps;
+  uint8_t* conv;
+  T* e_hist;
+  int max_sweeps;
+  double tol, tol_inner;
+  bool p_in_smem;
+};
+
+BF_DEV void atomic_max_pos(double* addr, double v) {
+  // non-negative doubles (incl. +inf) order like their bit patterns
+  atomicMax((unsigned long long*)addr, (unsigned long long)__double_as_longlong(v));
+}
+
+// scaled_offdiag (blockjacobi.py:57-76) of a square 2k x 2k matrix in smem, CTA-wide.
+template <typename T>
+BF_DEV double scaled_offdiag_cta(const T* G, int ld, int nn, double* red) {
+  if (threadIdx.x == 0) *red = 0.0;
+  __syncthreads();
+  double best = 0.0;
+  for (int e = threadIdx.x; e < nn * nn; e += blockDim.x) {
+    int j = e / nn, i = e % nn;
+    if (i == j) continue;
+    T di = (T)sqrt((double)fabs((double)G[(size_t)i * ld + i]));
+    T dj = (T)sqrt((double)fabs((double)G[(size_t)j * ld + j]));
+    T den = di * dj;
+    T num = G[(size_t)j * ld + i];
+    num = num < T(0) ? -num : num;
+    double rt = den > T(0) ? (double)(num / den) : (num > T(0) ? __longlong_as_double(0x7ff0000000000000LL) : 0.0);
+    best = rt > best ? rt : best;
+  }
+  best = warp_allreduce_max(best);
+  if ((threadIdx.x & 31) == 0 && best > 0.0) atomic_max_pos(red, best);
+  __syncthreads();
+  double r = *red;
+  __syncthreads();
+  return r;
+}
+
+// column c (0..2k-1) of the block pair -> global column
+BF_DEV int pair_col(int c, int k, int bi, int bj) { return c < k ? bi * k + c : bj * k + (c - k); }
+
+// rows x 2k panel of M (ld) times R (2k x 2k, smem): out = panel @ R, in place, row chunks
+// through smem. zero_sig: zero output columns whose sigma == 0 (gram path).
+template <typename T>
+BF_DEV void pair_times_rot(T* M, int ld, int rows, int k, int bi, int bj, const T* R, T* chunk, const T* sig,
+                           bool zero_null) {
+  const int kk = 2 * k;
+  const int CH = 32;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  for (int r0 = 0; r0 < rows; r0 += CH) {
+    int nr = rows - r0 < CH ? rows - r0 : CH;
+    for (int e = tid; e < kk * CH; e += nth) {
+      int c = e / CH, r = e % CH;
+      chunk[c * CH + r] = r < nr ? M[(size_t)pair_col(c, k, bi, bj) * ld + r0 + r] : T(0);
+    }
+    __syncthreads();
+    for (int e = tid; e < kk * CH; e += nth) {
+      int t = e / CH, r = e % CH;
+      if (r >= nr) continue;
+      T acc = 0;
+      for (int u = 0; u < kk; ++u) acc = fma(chunk[u * CH + r], R[(size_t)t * kk + u], acc);
+      if (zero_null && !(sig[t] != T(0))) acc = T(0);
+      M[(size_t)pair_col(t, k, bi, bj) * ld + r0 + r] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) bj_gram_step(BJArgs<T> a, int step) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int P = a.nb / 2;
+  const int64_t b = blockIdx.x / P;
+  const int pk = blockIdx.x % P;
+  if (b >= a.batch || !a.active[b]) return;
+  int bi, bj;
+  rr_pair(a.nb, step, pk, bi, bj);
+  const int k = a.k, kk = 2 * k, m = a.m, tid = threadIdx.x;
+  T* G = reinterpret_cast<T*>(smem_raw);  // kk x kk; inner W
+  T* U = G + kk * kk;                     // kk x kk rotation
+  T* chunk = U + kk * kk;                 // kk x 32
+  T* sig = chunk + kk * 32;               // kk
+  T* cand = sig + kk;                     // 2 kk
+  int* order = reinterpret_cast<int*>(cand + 2 * kk);
+  int* counters = order + kk;
+  double* red = reinterpret_cast<double*>(((uintptr_t)(counters + 4) + 7) & ~(uintptr_t)7);
+  T* Wb = a.W + b * (int64_t)m * a.n_pad;
+
+  // ---- G = pair^T pair, rows streamed in chunks of 32 (syrk, core.py:68-78)
+  for (int e = tid; e < kk * kk; e += blockDim.x) G[e] = T(0);
+  T acc[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) acc[q] = T(0);
+  const int ne = kk * kk;
+  for (int r0 = 0; r0 < m; r0 += 32) {
+    int nr = m - r0 < 32 ? m - r0 : 32;
+    __syncthreads();
+    for (int e = tid; e < kk * 32; e += blockDim.x) {
+      int c = e / 32, r = e % 32;
+      chunk[c * 32 + r] = r < nr ? Wb[(size_t)pair_col(c, k, bi, bj) * m + r0 + r] : T(0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      int e = tid + q * 256;
+      if (e < ne) {
+        int j = e / kk, i = e % kk;
+        if (i <= j) {
+          T s = acc[q];
+          for (int r = 0; r < 32; ++r) s = fma(chunk[i * 32 + r], chunk[j * 32 + r], s);
+          acc[q] = s;
+        }
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    int e = tid + q * 256;
+    if (e < ne) {
+      int j = e / kk, i = e % kk;
+      if (i <= j) {
+        G[(size_t)j * kk + i] = acc[q];
+        G[(size_t)i * kk + j] = acc[q];
+      }
+    }
+  }
+  __syncthreads();
+  // ---- convergence measure before the update (blockjacobi.py:126-129)
+  double e = scaled_offdiag_cta<T>(G, kk, kk, red);
+  if (tid == 0) atomic_max_pos(a.e_sweep + b, e);
+  if (e <= a.tol) return;
+  // ---- inner round-robin SVD of G without V (blockjacobi.py:130, _inner_options :79-81)
+  jacobi_sweeps<T, 4>(G, kk, (T*)nullptr, kk, kk, kk, kk, 1, a.tol_inner, 30, counters);
+  extract_svd_cta<T>(G, kk, (const T*)nullptr, kk, kk, kk, kk, 0, U, kk, sig, (T*)nullptr, kk, chunk, order, cand,
+                     counters + 2);
+  // (extract used `chunk` as its unsorted-norm scratch; `sig` holds the sorted sigma)
+  pair_times_rot<T>(Wb, m, m, k, bi, bj, U, chunk, sig, true);
+  if (a.V) pair_times_rot<T>(a.V + b * (int64_t)a.n_pad * a.n_pad, a.n_pad, a.n_pad, k, bi, bj, U, chunk, sig, false);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) bj_direct_step(BJArgs<T> a, int step) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int P = a.nb / 2;
+  const int64_t b = blockIdx.x / P;
+  const int pk = blockIdx.x % P;
+  if (b >= a.batch || !a.active[b]) return;
+  int bi, bj;
+  rr_pair(a.nb, step, pk, bi, bj);
+  const int k = a.k, kk = 2 * k, m = a.m, tid = threadIdx.x;
+  T* Rw = reinterpret_cast<T*>(smem_raw);  // kk x kk inner W (R)
+  T* Vi = Rw + kk * kk;                    // kk x kk inner V
+  T* Vr = Vi + kk * kk;                    // kk x kk rotation V_R
+  T* Ur = Vr + kk * kk;                    // kk x kk U_R (scaled later)
+  T* sig = Ur + kk * kk;                   // kk
+  T* sig2 = sig + kk;                      // kk (sorted sigma)
+  T* tau = sig2 + kk;                      // kk
+  T* cand = tau + kk;                      // 2 kk
+  int* order = reinterpret_cast<int*>(cand + 2 * kk);
+  int* counters = order + kk;
+  double* red = reinterpret_cast<double*>(((uintptr_t)(counters + 4) + 7) & ~(uintptr_t)7);
+  T* Pm = a.p_in_smem ? reinterpret_cast<T*>(red + 2) : a.P + (int64_t)blockIdx.x * m * kk;
+  T* Wb = a.W + b * (int64_t)m * a.n_pad;
+
+  for (int e = tid; e < m * kk; e += blockDim.x) {
+    int c = e / m, r = e % m;
+    Pm[e] = Wb[(size_t)pair_col(c, k, bi, bj) * m + r];
+  }
+  __syncthreads();
+  qr_factor_cta<T, 4>(Pm, m, m, kk, tau);  // qr(pair) (blockjacobi.py:136)
+  for (int e = tid; e < kk * kk; e += blockDim.x) {
+    int j = e / kk, i = e % kk;
+    Rw[e] = i <= j ? Pm[(size_t)j * m + i] : T(0);
+    Vi[e] = i == j ? T(1) : T(0);
+  }
+  __syncthreads();
+  double e = scaled_offdiag_cta<T>(Rw, kk, kk, red);
+  if (tid == 0) atomic_max_pos(a.e_sweep + b, e);
+  if (e <= a.tol) return;
+  jacobi_sweeps<T, 4>(Rw, kk, Vi, kk, kk, kk, kk, 1, a.tol_inner, 30, counters);
+  extract_svd_cta<T>(Rw, kk, Vi, kk, kk, kk, kk, kk, Ur, kk, sig2, Vr, kk, sig, order, cand, counters + 2);
+  // new pair = H_0 ... H_{kk-1} [U_R diag(sigma); 0]  (== (Q @ U_R) * sigma, blockjacobi.py:143)
+  for (int e2 = tid; e2 < m * kk; e2 += blockDim.x) {
+    int c = e2 / m, r = e2 % m;
+    Wb[(size_t)pair_col(c, k, bi, bj) * m + r] = r < kk ? Ur[(size_t)c * kk + r] * sig2[c] : T(0);
+  }
+  __syncthreads();
+  {
+    const int lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+    for (int j = kk - 1; j >= 0; --j) {
+      const T tj = tau[j];
+      if (tj == T(0)) continue;
+      const T* v = Pm + (size_t)j * m;
+      for (int c = warp; c < kk; c += nwarps) {
+        T* col = Wb + (size_t)pair_col(c, k, bi, bj) * m;
+        T d = 0;
+        for (int i = j + 1 + lane; i < m; i += 32) d = fma(v[i], col[i], d);
+        d = warp_allreduce_sum(d);
+        T w = (col[j] + d) * tj;
+        __syncwarp();
+        for (int i = j + 1 + lane; i < m; i += 32) col[i] = fma(-v[i], w, col[i]);
+        if (lane == 0) col[j] -= w;
+      }
+      __syncthreads();
+    }
+  }
+  if (a.V) pair_times_rot<T>(a.V + b * (int64_t)a.n_pad * a.n_pad, a.n_pad, a.n_pad, k, bi, bj, Vr, Ur, sig2, false);
+}
+
+template <typename T>
+__global__ void bj_init(BJArgs<T> a, const T* A) {
+  const int64_t b = blockIdx.x;
+  if (b >= a.batch) return;
+  const int m = a.m, n = a.n, np = a.n_pad;
+  T* Wb = a.W + b * (int64_t)m * np;
+  const T* Ab = A + b * (int64_t)m * n;
+  for (int64_t e = threadIdx.x; e < (int64_t)m * np; e += blockDim.x) Wb[e] = e < (int64_t)m * n ? Ab[e] : T(0);
+  if (a.V) {
+    T* Vb = a.V + b * (int64_t)np * np;
+    for (int64_t e = threadIdx.x; e < (int64_t)np * np; e += blockDim.x) Vb[e] = (e / np == e % np) ? T(1) : T(0);
+  }
+  if (threadIdx.x == 0) {
+    a.active[b] = 1;
+    a.e_sweep[b] = 0.0;
+    a.sweeps[b] = 0;
+    a.conv[b] = 0;
+  }
+}
+
+template <typename T>
+__global__ void bj_finalize_sweep(BJArgs<T> a) {
+  int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.batch || !a.active[b]) return;
+  double e = a.e_sweep[b];
+  int s = a.sweeps[b];
+  if (a.e_hist) a.e_hist[b * a.max_sweeps + s] = (T)e;
+  s += 1;
+  a.sweeps[b] = s;
+  if (e < a.tol) {
+    a.conv[b] = 1;
+    a.active[b] = 0;
+  } else if (s >= a.max_sweeps) {
+    a.active[b] = 0;
+  }
+  a.e_sweep[b] = 0.0;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) bj_extract(BJArgs<T> a, T* U, T* S, T* Vout, T* cand_g) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int64_t b = blockIdx.x;
+  if (b >= a.batch) return;
+  const int m = a.m, n = a.n, np = a.n_pad;
+  T* sig = reinterpret_cast<T*>(smem_raw);
+  int* order = reinterpret_cast<int*>(sig + np);
+  int* flag = order + np;
+  extract_svd_cta<T>(a.W + b * (int64_t)m * np, m, a.V ? a.V + b * (int64_t)np * np : nullptr, np, m, np, n, n,
+                     U + b * (int64_t)m * n, m, S + b * (int64_t)n, Vout ? Vout + b * (int64_t)n * n : nullptr, n,
+                     sig, order, cand_g + b * 2 * (int64_t)m, flag);
+}
+
+static void bj_geometry(int m, int n, int bw, int method, int& k, int& n_pad, int& nb) {
+  k = bw;
+  if (method == 1) {
+    k = m / 2 < k ? m / 2 : k;
+    if (k < 1) k = 1;
+  }
+  n_pad = ((n + 2 * k - 1) / (2 * k)) * (2 * k);
+  if (n_pad < 2 * k) n_pad = 2 * k;
+  nb = n_pad / k;
+}
+
+template <typename T>
+static size_t direct_smem(int m, int kk, bool p_in) {
+  size_t b = (size_t)4 * kk * kk * sizeof(T) + (size_t)5 * kk * sizeof(T) + (size_t)kk * sizeof(int) + 64;
+  if (p_in) b += (size_t)m * kk * sizeof(T);
+  return (b + 15) & ~(size_t)15;
+}
+
+template <typename T>
+struct BJLayout {
+  size_t w, v, p, e, act, cand, total;
+};
+
+template <typename T>
+static BJLayout<T> bj_layout(int64_t batch, int m, int n, int bw, int method, bool accv) {
+  int k, np, nb;
+  bj_geometry(m, n, bw, method, k, np, nb);
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  BJLayout<T> L;
+  size_t off = 0;
+  L.w = off;
+  off += al((size_t)batch * m * np * sizeof(T));
+  L.v = off;
+  off += accv ? al((size_t)batch * np * np * sizeof(T)) : 0;
+  L.p = off;
+  bool p_in = direct_smem<T>(m, 2 * k, true) <= 227 * 1024;
+  off += (method == 1 && !p_in) ? al((size_t)batch * (nb / 2) * m * 2 * k * sizeof(T)) : 0;
+  L.e = off;
+  off += al((size_t)batch * sizeof(double));
+  L.act = off;
+  off += al((size_t)batch);
+  L.cand = off;
+  off += al((size_t)batch * 2 * m * sizeof(T));
+  L.total = off;
+  return L;
+}
+
+size_t block_ws_bytes(int dtype, int64_t batch, int m, int n, int block_width, int method, bool accv) {
+  return dtype == 0 ? bj_layout<double>(batch, m, n, block_width, method, accv).total
+                    : bj_layout<float>(batch, m, n, block_width, method, accv).total;
+}
+
+template <typename T>
+static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
+  BJArgs<T> a;
+  int k, np, nb;
+  bj_geometry(L.m, L.n, L.block_width, L.method, k, np, nb);
+  BJLayout<T> lay = bj_layout<T>(L.batch, L.m, L.n, L.block_width, L.method, L.v != nullptr);
+  char* base = (char*)ws;
+  a.batch = L.batch;
+  a.m = L.m;
+  a.n = L.n;
+  a.n_pad = np;
+  a.k = k;
+  a.nb = nb;
+  a.W = (T*)(base + lay.w);
+  a.V = L.v ? (T*)(base + lay.v) : nullptr;
+  a.P = (T*)(base + lay.p);
+  a.e_sweep = (double*)(base + lay.e);
+  a.active = (uint8_t*)(base + lay.act);
+  a.sweeps = L.sweeps;
+  a.conv = L.converged;
+  a.e_hist = (T*)L.e_history;
+  a.max_sweeps = L.max_sweeps;
+  a.tol = L.tol;
+  a.tol_inner = sizeof(T) == 8 ? Tol<double>::svd : Tol<float>::svd;
+  const int kk = 2 * k;
+  a.p_in_smem = direct_smem<T>(L.m, kk, true) <= 227 * 1024;
+  cudaError_t e;
+  bj_init<T><<<(unsigned)L.batch, 256, 0, st>>>(a, (const T*)L.a);
+  if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
+  const unsigned grid = (unsigned)(L.batch * (nb / 2));
+  size_t smem;
+  if (L.method == 0) {
+    smem = (size_t)(2 * kk * kk + kk * 32 + 3 * kk) * sizeof(T) + (size_t)kk * sizeof(int) + 64;
+    e = cudaFuncSetAttribute(bj_gram_step<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  } else {
+    smem = direct_smem<T>(L.m, kk, a.p_in_smem);
+    e = cudaFuncSetAttribute(bj_direct_step<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  if (e != cudaSuccess) return (int)e;
+  for (int sw = 0; sw < L.max_sweeps; ++sw) {
+    for (int s = 0; s < nb - 1; ++s) {
+      if (L.method == 0)
+        bj_gram_step<T><<<grid, 256, smem, st>>>(a, s);
+      else
+        bj_direct_step<T><<<grid, 256, smem, st>>>(a, s);
+    }
+    bj_finalize_sweep<T><<<(unsigned)((L.batch + 255) / 256), 256, 0, st>>>(a);
+  }
+  if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
+  size_t xs = (size_t)np * (sizeof(T) + sizeof(int)) + 16;
+  e = cudaFuncSetAttribute(bj_extract<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xs);
+  if (e != cudaSuccess) return (int)e;
+  bj_extract<T><<<(unsigned)L.batch, 256, xs, st>>>(a, (T*)L.u, (T*)L.s, (T*)L.v, (T*)(base + lay.cand));
+  return (int)cudaGetLastError();
+}
+
+int launch_block_svd(int dtype, const BlockLaunch& L, void* ws, cudaStream_t st) {
+  if (L.batch == 0) return 0;
+  return dtype == 0 ? launch_block_t<double>(L, ws, st) : launch_block_t<float>(L, ws, st);
+}
+
+}  // namespace bf

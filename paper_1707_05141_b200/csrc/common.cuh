@@ -1,0 +1,115 @@
+// Shared device helpers for the batched factorisation kernels (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+#define BF_DEV __device__ __forceinline__
+
+namespace bf {
+
+constexpr unsigned FULL = 0xffffffffu;
+
+BF_DEV double shfl_xor(double v, int m) { return __shfl_xor_sync(FULL, v, m); }
+BF_DEV float shfl_xor(float v, int m) { return __shfl_xor_sync(FULL, v, m); }
+
+template <typename T>
+BF_DEV T warp_allreduce_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += shfl_xor(v, o);
+  return v;
+}
+
+template <typename T>
+BF_DEV T warp_allreduce_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    T w = shfl_xor(v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+// Fast reciprocal / reciprocal square root: MUFU seed + 2 Newton steps (~1 ulp).
+// Only used on arguments in the normal range (callers fall back otherwise).
+BF_DEV double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+BF_DEV double rsqrt_fast(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  // y <- y * (1.5 - 0.5 x y^2), twice
+  double hx = 0.5 * x;
+  double t = fma(-hx * y, y, 0.5);
+  y = fma(y, t, y);
+  t = fma(-hx * y, y, 0.5);
+  return fma(y, t, y);
+}
+
+// Rutishauser rotation (jacobi.py:68-80) for g_pq != 0:
+//   zeta = (g_qq - g_pp) / (2 g_pq); t = sign(zeta) / (|zeta| + hypot(1, zeta));
+//   c = 1 / hypot(1, t); s = c t.
+// Fast path with MUFU+Newton reciprocals; exact IEEE path for extreme ranges.
+BF_DEV void jacobi_rotation(double gpp, double gpq, double gqq, double& c, double& s) {
+  double den = 2.0 * gpq;
+  double diff = gqq - gpp;
+  double aden = fabs(den);
+  if (aden > 1e-290 && aden < 1e290 && fabs(diff) < 1e290) {
+    double zeta = diff * rcp_fast(den);
+    double az = fabs(zeta);
+    double t;
+    if (az < 1e150) {
+      double x = fma(az, az, 1.0);
+      double ry = rsqrt_fast(x);
+      double h = x * ry;  // sqrt(1 + zeta^2)
+      t = copysign(rcp_fast(az + h), zeta);
+    } else {
+      t = copysign(0.5 / az, zeta);  // az + hypot(1, az) == 2 az in double
+    }
+    c = rsqrt_fast(fma(t, t, 1.0));
+    s = c * t;
+  } else {
+    double zeta = diff / den;
+    double t = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
+    c = 1.0 / hypot(1.0, t);
+    s = c * t;
+  }
+}
+
+// Pair k of step st of the round-robin (circle method) schedule over nw columns
+// (jacobi.py:102-115): idx_t[0] = 0, idx_t[j] = 1 + ((j - 1 - t) mod (nw - 1)),
+// pair k = (idx_t[k], idx_t[nw-1-k]) normalised so p < q.
+BF_DEV void rr_pair(int nw, int st, int k, int& p, int& q) {
+  int L = nw - 1;
+  int a = (k == 0) ? 0 : 1 + (((k - 1 - st) % L) + L) % L;
+  int j = nw - 1 - k;
+  int b = 1 + (((j - 1 - st) % L) + L) % L;
+  p = a < b ? a : b;
+  q = a < b ? b : a;
+}
+
+// Serial (row-cyclic) ordering executed as its anti-diagonal wavefront: step s
+// (1 <= s <= 2nw-3) holds the disjoint pairs (p, s-p), p < s-p. Ordering pairs by
+// p+q respects every column dependency of the serial sweep (jacobi.py:127-129), so
+// the result is the serial sweep's, operation for operation.
+BF_DEV int wf_count(int nw, int s) {
+  int lo = s - (nw - 1);
+  lo = lo < 0 ? 0 : lo;
+  int hi = (s - 1) >> 1;
+  return hi >= lo ? hi - lo + 1 : 0;
+}
+BF_DEV void wf_pair(int nw, int s, int k, int& p, int& q) {
+  int lo = s - (nw - 1);
+  lo = lo < 0 ? 0 : lo;
+  p = lo + k;
+  q = s - p;
+}
+
+}  // namespace bf

@@ -1,0 +1,86 @@
+// Internal launch interface between the C-ABI layer (api.cu) and the kernel TUs.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace bf {
+
+template <typename T>
+struct Tol;
+template <>
+struct Tol<double> {
+  // jacobi.py:22-25, blockjacobi.py:19-22
+  static constexpr double svd = 1e-14;
+  static constexpr double block = 1e-13;
+};
+template <>
+struct Tol<float> {
+  static constexpr double svd = 1e-6;
+  static constexpr double block = 1e-5;
+};
+
+struct SvdLaunch {
+  int64_t batch;
+  int m, n;
+  const void* a;     // batch x (m x n) column-major, stride m*n
+  int64_t a_stride;  // elements between consecutive matrices
+  void* u;           // batch x (m x n)
+  int64_t u_stride;
+  void* s;  // batch x n
+  int64_t s_stride;
+  void* v;  // batch x (n x n) or null
+  int64_t v_stride;
+  int32_t* sweeps;
+  uint8_t* converged;
+  int64_t* rotations;
+  double tol;
+  int max_sweeps, ordering, tier;
+  bool transpose_a;  // read A^T (a is n x m column-major) -- used by rsvd for R_B^T
+};
+
+struct GemmLaunch {
+  int64_t batch;
+  int M, N, K;
+  const void* a;
+  int lda;
+  int64_t a_stride;
+  bool ta;  // op(A) = A^T (A stored K x M)
+  const void* b;
+  int ldb;
+  int64_t b_stride;
+  bool tb;
+  void* c;
+  int ldc;
+  int64_t c_stride;
+};
+
+// all return 0 or a CUDA error code; dtype 0 = f64, 1 = f32
+size_t svd_global_ws_bytes(int dtype, int64_t batch, int m, int n, int ordering, bool accv, int tier);
+int launch_svd(int dtype, const SvdLaunch& L, void* ws, cudaStream_t st);
+int launch_qr(int dtype, int64_t batch, int m, int n, const void* a, int64_t a_stride, void* q, int64_t q_stride,
+              void* r, int64_t r_stride, void* ws, cudaStream_t st);
+size_t qr_global_ws_bytes(int dtype, int64_t batch, int m, int n);
+int launch_gemm(int dtype, const GemmLaunch& L, cudaStream_t st);
+int launch_gaussian_f64(int64_t batch, int rows, int cols, uint64_t seed_lo, uint64_t seed_hi, int64_t index_base,
+                        int seed_mode, uint64_t xor_mask, double* out, int64_t out_stride, cudaStream_t st);
+int launch_sign_fix_f64(int64_t batch, int m, int n, double* q, const double* r, cudaStream_t st);
+int launch_scale_cols_f64(int64_t batch, int m, int n, double* q, const double* sigma, cudaStream_t st);
+
+struct BlockLaunch {
+  int64_t batch;
+  int m, n;
+  const void* a;
+  void* u;
+  void* s;
+  void* v;
+  int32_t* sweeps;
+  uint8_t* converged;
+  void* e_history;  // batch x max_sweeps or null
+  int block_width, method, max_sweeps;
+  double tol;
+};
+size_t block_ws_bytes(int dtype, int64_t batch, int m, int n, int block_width, int method, bool accv);
+int launch_block_svd(int dtype, const BlockLaunch& L, void* ws, cudaStream_t st);
+
+}  // namespace bf

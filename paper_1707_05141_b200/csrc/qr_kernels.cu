@@ -1,0 +1,104 @@
+// Batched Householder QR with explicit reduced Q (reference: qr.py:63-100).
+// One CTA per matrix; the matrix is staged in shared memory (Householder panels
+// staged in SMEM), Q is formed in shared memory when it fits
+// and directly in the output otherwise.
+#include "internal.h"
+#include "qr_cta.cuh"
+
+namespace bf {
+
+template <typename T>
+struct QrArgs {
+  int64_t batch;
+  int m, n;
+  const T* a;
+  int64_t a_stride;
+  T* q;
+  int64_t q_stride;
+  T* r;
+  int64_t r_stride;
+  bool r_in_smem, q_in_smem;
+  T* gws;
+  int64_t gws_stride;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) qr_cta_kernel(QrArgs<T> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int64_t b = blockIdx.x;
+  if (b >= a.batch) return;
+  const int m = a.m, n = a.n, tid = threadIdx.x;
+  T* tau = reinterpret_cast<T*>(smem_raw);
+  T* Rw = a.r_in_smem ? tau + ((n + 1) & ~1) : a.gws + b * a.gws_stride;
+  T* Qout = a.q + b * a.q_stride;
+  T* Qw = a.q_in_smem ? (a.r_in_smem ? Rw + (size_t)m * n : tau + ((n + 1) & ~1)) : Qout;
+  const T* A = a.a + b * a.a_stride;
+  // vectorised staging of the column-major matrix
+  for (int64_t e = tid; e < (int64_t)m * n; e += blockDim.x) Rw[e] = A[e];
+  __syncthreads();
+  qr_factor_cta<T, 4>(Rw, m, m, n, tau);
+  qr_form_q_cta<T, 4>(Rw, m, tau, Qw, m, m, n);
+  T* Rout = a.r + b * a.r_stride;
+  for (int64_t e = tid; e < (int64_t)n * n; e += blockDim.x) {
+    int j = (int)(e / n), i = (int)(e % n);
+    Rout[e] = i <= j ? Rw[(size_t)j * m + i] : T(0);
+  }
+  if (a.q_in_smem)
+    for (int64_t e = tid; e < (int64_t)m * n; e += blockDim.x) Qout[e] = Qw[e];
+}
+
+template <typename T>
+static void qr_plan(int m, int n, bool& r_in, bool& q_in, size_t& smem) {
+  const size_t cap = 227 * 1024;
+  size_t base = (size_t)((n + 1) & ~1) * sizeof(T);
+  size_t mat = (size_t)m * n * sizeof(T);
+  r_in = base + mat <= cap;
+  q_in = base + (r_in ? mat : 0) + mat <= cap;
+  smem = base + (r_in ? mat : 0) + (q_in ? mat : 0);
+}
+
+size_t qr_global_ws_bytes(int dtype, int64_t batch, int m, int n) {
+  bool r_in, q_in;
+  size_t smem;
+  if (dtype == 0)
+    qr_plan<double>(m, n, r_in, q_in, smem);
+  else
+    qr_plan<float>(m, n, r_in, q_in, smem);
+  if (r_in) return 0;
+  size_t per = ((size_t)m * n * (dtype == 0 ? 8 : 4) + 255) & ~(size_t)255;
+  return per * (size_t)batch;
+}
+
+template <typename T>
+static int launch_qr_t(int64_t batch, int m, int n, const void* a, int64_t as, void* q, int64_t qs, void* r,
+                       int64_t rs, void* ws, cudaStream_t st) {
+  QrArgs<T> p;
+  p.batch = batch;
+  p.m = m;
+  p.n = n;
+  p.a = (const T*)a;
+  p.a_stride = as;
+  p.q = (T*)q;
+  p.q_stride = qs;
+  p.r = (T*)r;
+  p.r_stride = rs;
+  size_t smem;
+  qr_plan<T>(m, n, p.r_in_smem, p.q_in_smem, smem);
+  p.gws = (T*)ws;
+  p.gws_stride = (int64_t)((((size_t)m * n * sizeof(T) + 255) & ~(size_t)255) / sizeof(T));
+  int nwarps = (n + 3) / 4;
+  nwarps = nwarps < 2 ? 2 : (nwarps > 8 ? 8 : nwarps);
+  cudaError_t e = cudaFuncSetAttribute(qr_cta_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  qr_cta_kernel<T><<<(unsigned)batch, nwarps * 32, smem, st>>>(p);
+  return (int)cudaGetLastError();
+}
+
+int launch_qr(int dtype, int64_t batch, int m, int n, const void* a, int64_t a_stride, void* q, int64_t q_stride,
+              void* r, int64_t r_stride, void* ws, cudaStream_t st) {
+  if (batch == 0 || n == 0) return 0;
+  return dtype == 0 ? launch_qr_t<double>(batch, m, n, a, a_stride, q, q_stride, r, r_stride, ws, st)
+                    : launch_qr_t<float>(batch, m, n, a, a_stride, q, q_stride, r, r_stride, ws, st);
+}
+
+}  // namespace bf

@@ -1,0 +1,158 @@
+// Batched one-sided Jacobi SVD: shared-memory tier (one CTA per matrix).
+//
+// Reference: svd() jacobi.py:231-284, batch_svd jacobi.py:287-290.
+// W and V are staged in shared memory when they fit (the paper's shared-memory
+// kernel); larger matrices keep them in an L2-resident global
+// workspace with the same code. The register tier (n <= 32) lives in svd_reg.cu.
+#include "internal.h"
+#include "jacobi_cta.cuh"
+
+namespace bf {
+
+template <typename T>
+struct SvdArgs {
+  int64_t batch;
+  int m, n, nw;
+  const T* a;
+  int64_t a_stride;
+  bool ta;
+  T* u;
+  int64_t u_stride;
+  T* s;
+  int64_t s_stride;
+  T* v;
+  int64_t v_stride;
+  int32_t* sweeps;
+  uint8_t* conv;
+  int64_t* rots;
+  double tol;
+  int max_sweeps, ordering;
+  bool in_smem;
+  T* gws;  // per-matrix global workspace when !in_smem
+  int64_t gws_stride;
+};
+
+template <typename T>
+__host__ __device__ static size_t svd_work_elems(int m, int nw, bool accv) {
+  return (size_t)m * nw + (accv ? (size_t)nw * nw : 0) + 2 * (size_t)m;
+}
+
+template <typename T>
+static size_t svd_smem_bytes(int m, int nw, bool accv, bool in_smem) {
+  size_t b = 0;
+  if (in_smem) b += svd_work_elems<T>(m, nw, accv) * sizeof(T);
+  b += (size_t)nw * sizeof(T) + (size_t)nw * sizeof(int) + 4 * sizeof(int) + sizeof(double) + 16;
+  return (b + 15) & ~(size_t)15;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512) svd_cta_kernel(SvdArgs<T> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int64_t b = blockIdx.x;
+  if (b >= a.batch) return;
+  const int m = a.m, n = a.n, nw = a.nw;
+  const bool accv = a.v != nullptr;
+  T* base = a.in_smem ? reinterpret_cast<T*>(smem_raw) : a.gws + b * a.gws_stride;
+  T* W = base;
+  T* V = accv ? W + (size_t)m * nw : nullptr;
+  T* cand = W + (size_t)m * nw + (accv ? (size_t)nw * nw : 0);
+  unsigned char* tail = smem_raw + (a.in_smem ? svd_work_elems<T>(m, nw, accv) * sizeof(T) : 0);
+  T* sig = reinterpret_cast<T*>(tail);
+  int* order = reinterpret_cast<int*>(sig + nw);
+  int* counters = order + nw;  // 4 ints
+  double* red = reinterpret_cast<double*>(((uintptr_t)(counters + 4) + 7) & ~(uintptr_t)7);
+
+  const T* A = a.a + b * a.a_stride;
+  const int tid = threadIdx.x;
+  if (!a.ta) {
+    for (int64_t e = tid; e < (int64_t)m * nw; e += blockDim.x) W[e] = e < (int64_t)m * n ? A[e] : T(0);
+  } else {  // A stored n x m column-major; W = A^T
+    for (int64_t e = tid; e < (int64_t)m * nw; e += blockDim.x) {
+      int j = (int)(e / m), i = (int)(e % m);
+      W[e] = j < n ? A[(size_t)i * n + j] : T(0);
+    }
+  }
+  if (accv)
+    for (int64_t e = tid; e < (int64_t)nw * nw; e += blockDim.x) V[e] = (e / nw == e % nw) ? T(1) : T(0);
+  __syncthreads();
+
+  SweepStats st = jacobi_sweeps<T, 4>(W, m, V, nw, m, n, nw, a.ordering, a.tol, a.max_sweeps, counters);
+  if (!st.converged) {
+    double off = off_orthogonality_cta<T>(W, m, m, nw, sig, red);
+    st.converged = off < a.tol;
+  }
+  extract_svd_cta<T>(W, m, V, nw, m, n, n, n, a.u + b * a.u_stride, m, a.s + b * a.s_stride,
+                     accv ? a.v + b * a.v_stride : nullptr, n, sig, order, cand, counters + 2);
+  if (tid == 0) {
+    if (a.sweeps) a.sweeps[b] = st.sweeps;
+    if (a.conv) a.conv[b] = (uint8_t)st.converged;
+    if (a.rots) a.rots[b] = st.rotations;
+  }
+}
+
+static int working_cols(int n, int ordering) { return (ordering == 1 && (n & 1)) ? n + 1 : n; }
+
+static bool fits_smem(size_t bytes) { return bytes <= 227 * 1024; }
+
+size_t svd_global_ws_bytes(int dtype, int64_t batch, int m, int n, int ordering, bool accv, int tier) {
+  (void)tier;
+  int nw = working_cols(n, ordering);
+  size_t es = dtype == 0 ? 8 : 4;
+  size_t smem = dtype == 0 ? svd_smem_bytes<double>(m, nw, accv, true) : svd_smem_bytes<float>(m, nw, accv, true);
+  if (fits_smem(smem)) return 0;
+  size_t per = (dtype == 0 ? svd_work_elems<double>(m, nw, accv) : svd_work_elems<float>(m, nw, accv)) * es;
+  per = (per + 255) & ~(size_t)255;
+  return per * (size_t)batch;
+}
+
+int launch_svd_reg(int dtype, const SvdLaunch& L, cudaStream_t st, bool* handled);
+
+template <typename T>
+static int launch_svd_t(const SvdLaunch& L, void* ws, cudaStream_t st) {
+  SvdArgs<T> a;
+  a.batch = L.batch;
+  a.m = L.m;
+  a.n = L.n;
+  a.nw = working_cols(L.n, L.ordering);
+  a.a = (const T*)L.a;
+  a.a_stride = L.a_stride;
+  a.ta = L.transpose_a;
+  a.u = (T*)L.u;
+  a.u_stride = L.u_stride;
+  a.s = (T*)L.s;
+  a.s_stride = L.s_stride;
+  a.v = (T*)L.v;
+  a.v_stride = L.v_stride;
+  a.sweeps = L.sweeps;
+  a.conv = L.converged;
+  a.rots = L.rotations;
+  a.tol = L.tol;
+  a.max_sweeps = L.max_sweeps;
+  a.ordering = L.ordering;
+  const bool accv = L.v != nullptr;
+  size_t smem = svd_smem_bytes<T>(L.m, a.nw, accv, true);
+  a.in_smem = fits_smem(smem);
+  a.gws = (T*)ws;
+  size_t per = svd_work_elems<T>(L.m, a.nw, accv) * sizeof(T);
+  a.gws_stride = (int64_t)(((per + 255) & ~(size_t)255) / sizeof(T));
+  if (!a.in_smem) smem = svd_smem_bytes<T>(L.m, a.nw, accv, false);
+  int pairs = a.nw / 2 > 0 ? a.nw / 2 : 1;
+  int nwarps = (pairs + 3) / 4;
+  nwarps = nwarps < 2 ? 2 : (nwarps > 16 ? 16 : nwarps);
+  cudaError_t e = cudaFuncSetAttribute(svd_cta_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  svd_cta_kernel<T><<<(unsigned)L.batch, nwarps * 32, smem, st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+int launch_svd(int dtype, const SvdLaunch& L, void* ws, cudaStream_t st) {
+  if (L.batch == 0) return 0;
+  if (L.tier != 2 && !L.transpose_a) {
+    bool handled = false;
+    int rc = launch_svd_reg(dtype, L, st, &handled);
+    if (handled || rc) return rc;
+  }
+  return dtype == 0 ? launch_svd_t<double>(L, ws, st) : launch_svd_t<float>(L, ws, st);
+}
+
+}  // namespace bf
