@@ -90,7 +90,8 @@ int svd_impl(int64_t batch, int m, int n, const T* a, T* u, T* s, T* v, int32_t*
     }
     return cuda_rc((int)cudaGetLastError(), "svd");
   }
-  rc = check_ws(ws, wsb, bf::svd_global_ws_bytes(dt, batch, m, n, o->ordering, o->accumulate_v != 0, o->tier));
+  rc = check_ws(ws, wsb,
+                bf::svd_global_ws_bytes(dt, batch, m, n, o->ordering, o->accumulate_v != 0, o->tier, o->max_sweeps));
   if (rc) return rc;
   bf::SvdLaunch L;
   L.batch = batch;
@@ -112,7 +113,7 @@ int svd_impl(int64_t batch, int m, int n, const T* a, T* u, T* s, T* v, int32_t*
   L.ordering = o->ordering;
   L.tier = o->tier;
   L.transpose_a = false;
-  return cuda_rc(bf::launch_svd(dt, L, ws, S(st)), "svd");
+  return cuda_rc(bf::launch_svd(dt, L, ws, wsb, S(st)), "svd");
 }
 
 // ---------------------------------------------------------------- block SVD
@@ -183,7 +184,7 @@ RsvdLayout rsvd_layout(int64_t batch, int m, int n, int w, int es, bool need_ome
   L.vr = take((size_t)batch * w * w);
   size_t qws = std::max(bf::qr_global_ws_bytes(es == 8 ? 0 : 1, batch, m, w),
                         bf::qr_global_ws_bytes(es == 8 ? 0 : 1, batch, n, w));
-  size_t sws = bf::svd_global_ws_bytes(es == 8 ? 0 : 1, batch, w, w, 1, true, 0);
+  size_t sws = bf::svd_global_ws_bytes(es == 8 ? 0 : 1, batch, w, w, 1, true, 0, 30);
   L.svdws = off;
   off += al(std::max(qws, sws));
   L.total = off;
@@ -257,7 +258,7 @@ int rsvd_impl(int64_t batch, int m, int n, int k, int p, uint64_t slo, uint64_t 
   L.ordering = 1;
   L.tier = 0;
   L.transpose_a = true;
-  if ((rc = bf::launch_svd(dt, L, sws, cs))) return cuda_rc(rc, "rsvd/svd");
+  if ((rc = bf::launch_svd(dt, L, sws, Ly.total - Ly.svdws, cs))) return cuda_rc(rc, "rsvd/svd");
   // U = Q @ U_R, V = Q_B @ V_R (rsvd.py:74-75)
   g = bf::GemmLaunch{batch, m, w, w, Q, m, (int64_t)m * w, false, Ur, w, (int64_t)w * w, false, u, m, (int64_t)m * w};
   if ((rc = bf::launch_gemm(dt, g, cs))) return cuda_rc(rc, "rsvd/gemm3");
@@ -288,7 +289,8 @@ int bf_qr_batched_f32(int64_t batch, int32_t m, int32_t n, const float* a, float
 
 size_t bf_svd_workspace_size(int64_t batch, int32_t m, int32_t n, int32_t es, const bf_jacobi_opts* o) {
   if (!o || m < n || n <= 0) return 0;
-  return bf::svd_global_ws_bytes(es == 8 ? 0 : 1, batch, m, n, o->ordering, o->accumulate_v != 0, o->tier);
+  return bf::svd_global_ws_bytes(es == 8 ? 0 : 1, batch, m, n, o->ordering, o->accumulate_v != 0, o->tier,
+                                 o->max_sweeps);
 }
 int bf_svd_batched_f64(int64_t batch, int32_t m, int32_t n, const double* a, double* u, double* s, double* v,
                        int32_t* sweeps, uint8_t* conv, int64_t* rots, const bf_jacobi_opts* o, void* ws, size_t wsb,

@@ -56,8 +56,8 @@ struct GemmLaunch {
 };
 
 // all return 0 or a CUDA error code; dtype 0 = f64, 1 = f32
-size_t svd_global_ws_bytes(int dtype, int64_t batch, int m, int n, int ordering, bool accv, int tier);
-int launch_svd(int dtype, const SvdLaunch& L, void* ws, cudaStream_t st);
+size_t svd_global_ws_bytes(int dtype, int64_t batch, int m, int n, int ordering, bool accv, int tier, int max_sweeps);
+int launch_svd(int dtype, const SvdLaunch& L, void* ws, size_t ws_bytes, cudaStream_t st);
 int launch_qr(int dtype, int64_t batch, int m, int n, const void* a, int64_t a_stride, void* q, int64_t q_stride,
               void* r, int64_t r_stride, void* ws, cudaStream_t st);
 size_t qr_global_ws_bytes(int dtype, int64_t batch, int m, int n);

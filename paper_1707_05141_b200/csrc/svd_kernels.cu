@@ -94,8 +94,9 @@ static int working_cols(int n, int ordering) { return (ordering == 1 && (n & 1))
 
 static bool fits_smem(size_t bytes) { return bytes <= 227 * 1024; }
 
-size_t svd_global_ws_bytes(int dtype, int64_t batch, int m, int n, int ordering, bool accv, int tier) {
-  (void)tier;
+size_t svd_reg_ws_bytes(int dtype, const SvdLaunch& L);
+
+static size_t svd_shared_ws_bytes(int dtype, int64_t batch, int m, int n, int ordering, bool accv) {
   int nw = working_cols(n, ordering);
   size_t es = dtype == 0 ? 8 : 4;
   size_t smem = dtype == 0 ? svd_smem_bytes<double>(m, nw, accv, true) : svd_smem_bytes<float>(m, nw, accv, true);
@@ -105,7 +106,21 @@ size_t svd_global_ws_bytes(int dtype, int64_t batch, int m, int n, int ordering,
   return per * (size_t)batch;
 }
 
-int launch_svd_reg(int dtype, const SvdLaunch& L, cudaStream_t st, bool* handled);
+size_t svd_global_ws_bytes(int dtype, int64_t batch, int m, int n, int ordering, bool accv, int tier, int max_sweeps) {
+  SvdLaunch L{};
+  L.batch = batch;
+  L.m = m;
+  L.n = n;
+  L.ordering = ordering;
+  L.tier = tier;
+  L.max_sweeps = max_sweeps;
+  L.v = accv ? (void*)1 : nullptr;
+  size_t r = svd_reg_ws_bytes(dtype, L);
+  size_t s = svd_shared_ws_bytes(dtype, batch, m, n, ordering, accv);
+  return r > s ? r : s;
+}
+
+int launch_svd_reg(int dtype, const SvdLaunch& L, void* ws, size_t wsb, cudaStream_t st, bool* handled);
 
 template <typename T>
 static int launch_svd_t(const SvdLaunch& L, void* ws, cudaStream_t st) {
@@ -145,11 +160,11 @@ static int launch_svd_t(const SvdLaunch& L, void* ws, cudaStream_t st) {
   return (int)cudaGetLastError();
 }
 
-int launch_svd(int dtype, const SvdLaunch& L, void* ws, cudaStream_t st) {
+int launch_svd(int dtype, const SvdLaunch& L, void* ws, size_t ws_bytes, cudaStream_t st) {
   if (L.batch == 0) return 0;
-  if (L.tier != 2 && !L.transpose_a) {
+  if (L.tier != 2) {
     bool handled = false;
-    int rc = launch_svd_reg(dtype, L, st, &handled);
+    int rc = launch_svd_reg(dtype, L, ws, ws_bytes, st, &handled);
     if (handled || rc) return rc;
   }
   return dtype == 0 ? launch_svd_t<double>(L, ws, st) : launch_svd_t<float>(L, ws, st);
