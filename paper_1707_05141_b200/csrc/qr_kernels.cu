@@ -94,9 +94,15 @@ static int launch_qr_t(int64_t batch, int m, int n, const void* a, int64_t as, v
   return (int)cudaGetLastError();
 }
 
+int launch_qr_reg(int dtype, int64_t batch, int m, int n, const void* a, int64_t as, void* q, int64_t qs, void* r,
+                  int64_t rs, cudaStream_t st);
+
 int launch_qr(int dtype, int64_t batch, int m, int n, const void* a, int64_t a_stride, void* q, int64_t q_stride,
               void* r, int64_t r_stride, void* ws, cudaStream_t st) {
   if (batch == 0 || n == 0) return 0;
+  // register-resident warp-per-matrix path for the instantiated shapes
+  int rc = launch_qr_reg(dtype, batch, m, n, a, a_stride, q, q_stride, r, r_stride, st);
+  if (rc != -1) return rc;
   return dtype == 0 ? launch_qr_t<double>(batch, m, n, a, a_stride, q, q_stride, r, r_stride, ws, st)
                     : launch_qr_t<float>(batch, m, n, a, a_stride, q, q_stride, r, r_stride, ws, st);
 }
