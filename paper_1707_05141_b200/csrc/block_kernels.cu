@@ -16,6 +16,7 @@
 #include "internal.h"
 #include "jacobi_cta.cuh"
 #include "qr_cta.cuh"
+#include "block_gemm.cuh"
 
 namespace bf {
 
@@ -310,8 +311,11 @@ static size_t direct_smem(int m, int kk, bool p_in) {
 
 template <typename T>
 struct BJLayout {
-  size_t w, v, p, e, act, cand, total;
+  size_t w, v, p, e, act, cand, g, u, s, pact, iws, total;
 };
+
+// batched Gram pipeline (bj_gram -> register-tier inner SVD -> bj_rot) covers 2k in {16,32,48,64}
+static bool bj_batched_gram(int method, int kk) { return method == 0 && kk % 16 == 0 && kk <= 64; }
 
 template <typename T>
 static BJLayout<T> bj_layout(int64_t batch, int m, int n, int bw, int method, bool accv) {
@@ -333,6 +337,19 @@ static BJLayout<T> bj_layout(int64_t batch, int m, int n, int bw, int method, bo
   off += al((size_t)batch);
   L.cand = off;
   off += al((size_t)batch * 2 * m * sizeof(T));
+  const int kk = 2 * k;
+  const int64_t slots = batch * (nb / 2);
+  const bool bg = bj_batched_gram(method, kk);
+  L.g = off;
+  off += bg ? al((size_t)slots * kk * kk * sizeof(T)) : 0;
+  L.u = off;
+  off += bg ? al((size_t)slots * kk * kk * sizeof(T)) : 0;
+  L.s = off;
+  off += bg ? al((size_t)slots * kk * sizeof(T)) : 0;
+  L.pact = off;
+  off += bg ? al((size_t)slots) : 0;
+  L.iws = off;
+  off += bg ? al(svd_global_ws_bytes(sizeof(T) == 8 ? 0 : 1, slots, kk, kk, 1, false, 0, 30)) : 0;
   L.total = off;
   return L;
 }
@@ -381,12 +398,75 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
     e = cudaFuncSetAttribute(bj_direct_step<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   }
   if (e != cudaSuccess) return (int)e;
+  const bool bg = bj_batched_gram(L.method, kk);
+  BJGemmArgs<T> g;
+  SvdLaunch in{};
+  size_t rot_smem = 0;
+  if (bg) {
+    g.batch = L.batch;
+    g.m = L.m;
+    g.n_pad = np;
+    g.k = k;
+    g.nb = nb;
+    g.W = a.W;
+    g.V = a.V;
+    g.G = (T*)(base + lay.g);
+    g.U = (T*)(base + lay.u);
+    g.S = (T*)(base + lay.s);
+    g.pair_act = (uint8_t*)(base + lay.pact);
+    g.active = a.active;
+    g.e_sweep = a.e_sweep;
+    g.tol = L.tol;
+    // inner SVD of every active G: round robin, no V, default tolerance (blockjacobi.py:79-81)
+    in.batch = L.batch * (nb / 2);
+    in.m = kk;
+    in.n = kk;
+    in.a = g.G;
+    in.a_stride = (int64_t)kk * kk;
+    in.u = g.U;
+    in.u_stride = (int64_t)kk * kk;
+    in.s = g.S;
+    in.s_stride = kk;
+    in.v = nullptr;
+    in.v_stride = 0;
+    in.sweeps = nullptr;
+    in.converged = nullptr;
+    in.rotations = nullptr;
+    in.tol = a.tol_inner;
+    in.max_sweeps = 30;
+    in.ordering = 1;
+    in.tier = 0;
+    in.transpose_a = false;
+    in.active = g.pair_act;
+    rot_smem = (size_t)2 * kk * (kk + 1) * sizeof(T);
+    const int TT = kk / 16;
+    if (TT == 1) e = cudaFuncSetAttribute(bj_rot<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rot_smem);
+    if (TT == 2) e = cudaFuncSetAttribute(bj_rot<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rot_smem);
+    if (TT == 3) e = cudaFuncSetAttribute(bj_rot<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rot_smem);
+    if (TT == 4) e = cudaFuncSetAttribute(bj_rot<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rot_smem);
+    if (e != cudaSuccess) return (int)e;
+  }
+  void* iws = base + lay.iws;
+  const size_t iws_bytes = lay.total - lay.iws;
   for (int sw = 0; sw < L.max_sweeps; ++sw) {
     for (int s = 0; s < nb - 1; ++s) {
-      if (L.method == 0)
+      if (bg) {
+        const int TT = kk / 16;
+        if (TT == 1) bj_gram<T, 1><<<grid, 256, 0, st>>>(g, s);
+        if (TT == 2) bj_gram<T, 2><<<grid, 256, 0, st>>>(g, s);
+        if (TT == 3) bj_gram<T, 3><<<grid, 256, 0, st>>>(g, s);
+        if (TT == 4) bj_gram<T, 4><<<grid, 256, 0, st>>>(g, s);
+        int rc = launch_svd(sizeof(T) == 8 ? 0 : 1, in, iws, iws_bytes, st);
+        if (rc) return rc;
+        if (TT == 1) bj_rot<T, 1><<<grid, 256, rot_smem, st>>>(g, s);
+        if (TT == 2) bj_rot<T, 2><<<grid, 256, rot_smem, st>>>(g, s);
+        if (TT == 3) bj_rot<T, 3><<<grid, 256, rot_smem, st>>>(g, s);
+        if (TT == 4) bj_rot<T, 4><<<grid, 256, rot_smem, st>>>(g, s);
+      } else if (L.method == 0) {
         bj_gram_step<T><<<grid, 256, smem, st>>>(a, s);
-      else
+      } else {
         bj_direct_step<T><<<grid, 256, smem, st>>>(a, s);
+      }
     }
     bj_finalize_sweep<T><<<(unsigned)((L.batch + 255) / 256), 256, 0, st>>>(a);
   }

@@ -37,6 +37,7 @@ struct SvdLaunch {
   double tol;
   int max_sweeps, ordering, tier;
   bool transpose_a;  // read A^T (a is n x m column-major) -- used by rsvd for R_B^T
+  const uint8_t* active = nullptr;  // optional per-entry mask: inactive entries are skipped
 };
 
 struct GemmLaunch {

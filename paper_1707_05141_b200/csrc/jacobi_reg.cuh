@@ -382,8 +382,8 @@ struct WAction {
     }
     recompute = __any_sync(FULL, flag);
     __syncwarp();
-    if (warp == 0 && mine && (CH == 2 || (lane & 1) == 0)) log[k] = make_double2(cs[2 * k], cs[2 * k + 1]);
-    log += NPAIR;
+    if (log != nullptr && warp == 0 && mine && (CH == 2 || (lane & 1) == 0)) log[k] = make_double2(cs[2 * k], cs[2 * k + 1]);
+    if (log != nullptr) log += NPAIR;
     G::template apply<T, KIND, PH>(w, cs);
     __syncwarp();
   }

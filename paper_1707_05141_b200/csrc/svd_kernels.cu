@@ -30,6 +30,7 @@ struct SvdArgs {
   bool in_smem;
   T* gws;  // per-matrix global workspace when !in_smem
   int64_t gws_stride;
+  const uint8_t* active;
 };
 
 template <typename T>
@@ -50,6 +51,7 @@ __global__ void __launch_bounds__(512) svd_cta_kernel(SvdArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int64_t b = blockIdx.x;
   if (b >= a.batch) return;
+  if (a.active && !a.active[b]) return;
   const int m = a.m, n = a.n, nw = a.nw;
   const bool accv = a.v != nullptr;
   T* base = a.in_smem ? reinterpret_cast<T*>(smem_raw) : a.gws + b * a.gws_stride;
@@ -144,6 +146,7 @@ static int launch_svd_t(const SvdLaunch& L, void* ws, cudaStream_t st) {
   a.tol = L.tol;
   a.max_sweeps = L.max_sweeps;
   a.ordering = L.ordering;
+  a.active = L.active;
   const bool accv = L.v != nullptr;
   size_t smem = svd_smem_bytes<T>(L.m, a.nw, accv, true);
   a.in_smem = fits_smem(smem);

@@ -31,8 +31,9 @@ struct RegArgs {
   int64_t* rots;
   double tol;
   int max_sweeps;
-  double2* log;  // gridDim.x slots of log_stride entries
+  double2* log;  // gridDim.x slots of log_stride entries (null without V)
   int64_t log_stride;
+  const uint8_t* active;  // optional: entries with active[b] == 0 are skipped
 };
 
 constexpr int kStage = 8;
@@ -74,6 +75,7 @@ __global__ void __launch_bounds__(C::threads) svd_reg_kernel(RegArgs<T> a) {
   const int row = warp * 32 + lane;
 
   for (int64_t b = blockIdx.x; b < a.batch; b += gridDim.x) {
+    if (a.active && !a.active[b]) continue;  // uniform across the CTA
     const T* A = a.a + b * a.a_stride;
     T w[NP];
 #pragma unroll
@@ -93,7 +95,7 @@ __global__ void __launch_bounds__(C::threads) svd_reg_kernel(RegArgs<T> a) {
     act.d = d_all + warp * 64;
     act.red = red;
     act.red2 = red2;
-    act.log = a.log + (int64_t)blockIdx.x * a.log_stride;
+    act.log = a.log ? a.log + (int64_t)blockIdx.x * a.log_stride : nullptr;
     act.sweeps = 0;
     act.conv = n < 2;
     act.rot = 0;
@@ -210,12 +212,12 @@ static int launch_reg(const SvdLaunch& L, void* ws, size_t ws_bytes, cudaStream_
   const int grid = (int)(L.batch < cap ? L.batch : cap);
   const int64_t log_stride =
       ((int64_t)L.max_sweeps * reg_steps_per_sweep(C::np, L.n, ORD) + kStage + 1) * C::pairs;
-  const size_t log_bytes = (size_t)grid * log_stride * sizeof(double2);
+  const size_t log_bytes = L.v ? (size_t)grid * log_stride * sizeof(double2) : 0;
   if (need) {
     *need = log_bytes;
     return 0;
   }
-  if (!ws || ws_bytes < log_bytes) return -2;
+  if (log_bytes && (!ws || ws_bytes < log_bytes)) return -2;
   RegArgs<T> a;
   a.batch = L.batch;
   a.m = L.m;
@@ -235,8 +237,9 @@ static int launch_reg(const SvdLaunch& L, void* ws, size_t ws_bytes, cudaStream_
   a.rots = L.rotations;
   a.tol = L.tol;
   a.max_sweeps = L.max_sweeps;
-  a.log = (double2*)ws;
+  a.log = L.v ? (double2*)ws : nullptr;
   a.log_stride = log_stride;
+  a.active = L.active;
   svd_reg_kernel<T, C, ORD><<<grid, C::threads, smem, st>>>(a);
   return (int)cudaGetLastError();
 }
