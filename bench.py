@@ -45,6 +45,16 @@ CONFIGS = {
 HEADLINE = "cfg3"
 
 
+def load_profile(name):
+    """Per-launch DRAM traffic of the config's dominant kernel from the committed ncu --set full
+    summary (profiles/ncu_full_r01.json, written by tools/ncu_summary.py)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_full_r01.json")))
+        return d.get(name, {})
+    except Exception:  # noqa: BLE001
+        return {}
+
+
 def load_peaks():
     peaks = {}
     try:
@@ -133,8 +143,10 @@ class ClockSampler:
 class GpuConfig:
     """Builds device-resident inputs for one config and runs its hot path once per step."""
 
-    def __init__(self, name, cfg, device, rank):
+    def __init__(self, name, cfg, device, rank, world=1):
         import torch
+
+        from paper_1707_05141_b200.shard import ShardPlan
 
         import paper_1707_05141_b200 as bf
         from paper_1707_05141_b200.blockjacobi import block_svd_colmajor
@@ -146,9 +158,12 @@ class GpuConfig:
         self.bf, self.torch = bf, torch
         self.name, self.cfg, self.dev = name, cfg, device
         m, n, B = cfg["m"], cfg["n"], cfg["batch"]
-        seed0 = cfg["seed"] + rank * B  # weak scaling: every rank its own batch
+        # weak scaling: a global batch of world*B entries, contiguous shard of B per rank
+        self.plan = ShardPlan(world * B, world, rank)
+        seed0 = cfg["seed"] + self.plan.start
         if cfg["kind"] == "rsvd":
-            self.a, _ = bf.make_matrix_tensor(B, m, n, 1e16, rank=64, seed=seed0, device=device)
+            self.a, _ = bf.make_matrix_tensor(B, m, n, 1e16, rank=64, seed=cfg["seed"], index_base=self.plan.start,
+                                              device=device)
         else:
             self.a = bf.gaussian_tensor(B, m, n, seed0, seed_mode="add", device=device)
         self.store = self.a.transpose(1, 2).contiguous()  # column-major storage, resident
@@ -168,7 +183,12 @@ class GpuConfig:
             self.out = self.k_block(self.store, m, n, opts)
         else:
             opts = bf.RsvdOptions(k=c["k"], p=c["p"], seed=5)
-            self.out = self.k_rsvd(self.store, m, n, opts, index_base=0)
+            self.out = self.k_rsvd(self.store, m, n, opts, index_base=self.plan.start)  # seed ^ global index
+
+    def kernel_name(self):
+        c = self.cfg
+        return {"svd": "svd_reg_kernel", "qr": "qr_reg_kernel", "block": "svd_reg_kernel (inner) + bj_rot + bj_gram",
+                "rsvd": "qr_reg_kernel + svd_reg_kernel + gemm_kernel"}[c["kind"]]
 
     def launches_per_step(self):
         c = self.cfg
@@ -217,7 +237,7 @@ class GpuConfig:
                 dev_in, m, n, bf.BlockJacobiOptions(method="gram", block_width=32, tolerance=1e-11, accumulate_v=True))
             outs = [r["u"], r["s"], r["v"], r["sweeps"], r["converged"]]
         else:
-            r = self.k_rsvd(dev_in, m, n, bf.RsvdOptions(k=c["k"], p=c["p"], seed=5))
+            r = self.k_rsvd(dev_in, m, n, bf.RsvdOptions(k=c["k"], p=c["p"], seed=5), index_base=self.plan.start)
             outs = [r["u"], r["s"], r["v"]]
         for o, p in zip(outs, pinned_out):
             p.copy_(o, non_blocking=True)
@@ -388,7 +408,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    gc = GpuConfig(name, cfg, device, rank)
+    gc = GpuConfig(name, cfg, device, rank, world)
     barrier()
     clocks = ClockSampler(local)
     clocks.start()
@@ -401,23 +421,40 @@ def main():
     value = world * B * args.steps / t_max
     flops, bytes_alg = gc.flops()
     ms = 1e3 * t_max / args.steps
-    achieved_tf = flops / (t_dev / args.steps) / 1e12
+    # the headline step is ONE launch of the dominant kernel on the current stream (the C-ABI
+    # call launches exactly one kernel for svd/qr), so the per-step CUDA-event time is the
+    # kernel's launch duration
+    t_launch = t_dev / args.steps
+    achieved_tf = flops / t_launch / 1e12
+    prof = load_profile(name)
     # e2e through the public API with host buffers
-    t_e2e, h2d, d2h = time_e2e(gc, max(1, min(args.steps, 3)))
+    e2e_steps = max(1, min(args.steps, 3))
+    t_e2e, h2d, d2h = time_e2e(gc, e2e_steps)
     e2e_v = max_over_ranks(t_e2e)
-    e2e_value = world * B * max(1, min(args.steps, 3)) / e2e_v
+    e2e_value = world * B * e2e_steps / e2e_v
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference Gaussian stream, generated on device)",
-            "config": workload, "gflops": flops / (t_dev / args.steps) / 1e9,
-            "roofline": {"bound": "fp64", "achieved": achieved_tf, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
-                         "frac": achieved_tf / peaks["fp64_tflops"], "traffic": None,
-                         "note": "FP64 peak = DMMA loop measured on this pool (profiles/fp64_peak_r01.json); "
-                                 "MEASURED_PEAKS.json has no FP64 entry. Algorithmic flops per SURVEY §8d from the "
-                                 "run's own sweep/rotation counters",
-                         "hbm_achieved_gbs": bytes_alg / (t_dev / args.steps) / 1e9, "hbm_peak_gbs": peaks["hbm_gbs"]},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+            "config": workload, "gflops": flops / t_launch / 1e9,
+            "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+                         "frac": achieved_tf / peaks["fp64_tflops"],
+                         "traffic": prof.get("dram_bytes_per_launch"),
+                         "kernel": prof.get("kernel", gc.kernel_name()),
+                         "launches_per_step": gc.launches_per_step(),
+                         "flops_per_launch": flops, "alg_bytes_per_launch": bytes_alg,
+                         "peak_source": "FP64 compute roof: FP64 tensor-core (DMMA) loop measured on this pool, "
+                                        "profiles/fp64_peak_r01.json (MEASURED_PEAKS.json has no FP64 entry); the "
+                                        "Jacobi kernels issue DFMA, whose measured peak is lower",
+                         "dfma_peak": peaks.get("fp64_dfma_tflops"),
+                         "frac_of_dfma": achieved_tf / peaks["fp64_dfma_tflops"] if peaks.get("fp64_dfma_tflops") else None,
+                         "flops_rule": "SURVEY §8d / PAPER.md:172: 6m per pair visit + (6m+6n) per rotation, from the "
+                                       "run's own per-matrix sweep and rotation counters",
+                         "traffic_source": prof.get("source"),
+                         "hbm_achieved_gbs": bytes_alg / t_launch / 1e9, "hbm_peak_gbs": peaks["hbm_gbs"]},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "path": "C-ABI call (svd_colmajor -> bf_svd_batched_f64) with pinned HOST buffers: H2D of A, "
+                            "D2H of U, sigma, V, sweeps, converged inside the timed region"},
             "gpu_launches": gc.launches_per_step() * args.steps, "clocks": clk}
     del gc
     torch.cuda.empty_cache()
@@ -430,7 +467,7 @@ def main():
         for other, oc in CONFIGS.items():
             if other == name:
                 continue
-            g2 = GpuConfig(other, oc, device, rank)
+            g2 = GpuConfig(other, oc, device, rank, world)
             barrier()
             st = 2 if oc["kind"] == "block" else 3
             t2 = time_gpu(g2, st, 1, flush)
