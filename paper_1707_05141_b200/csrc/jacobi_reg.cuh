@@ -15,65 +15,39 @@
 // Steps are unrolled by two with the data lagging one step in the second copy (compile-time
 // register remap), so positions physically move every other step.
 //
-// Per step only g_pq needs a cross-lane reduction: the column norms g_pp, g_qq are carried
+// Per step only g_pq needs a cross-row reduction: the column norms g_pp, g_qq are carried
 // per column (recomputed exactly at every sweep start, updated with the exact 2x2
 // eigenvalues d_p - t g_pq, d_q + t g_pq after each rotation, and recomputed whenever an
-// update cancels) -- LAPACK dgesvj's scheme. g_pq partials are reduced with a recursive-
-// halving shuffle tree (16 pairs per 16 shuffles); each pair's Rutishauser rotation
-// (jacobi.py:68-80) is computed by ONE lane (not redundantly per lane) with
-// the reference's skip rule (jacobi.py:134/167); (c, s) reach the other lanes through a
-// per-warp shared-memory slot, and are appended to a rotation log from which V is rebuilt
+// update cancels) -- LAPACK dgesvj's scheme. The row products are transposed through a
+// shared-memory buffer and summed by a few threads per pair (WAction below); each pair's
+// Rutishauser rotation (jacobi.py:68-80) is computed by that pair's threads only (not by
+// every lane) with the reference's skip rule (jacobi.py:134/167); (c, s) reach
+// the rows through shared memory and are appended to a rotation log from which V is rebuilt
 // afterwards (so V never occupies registers during the sweeps).
 #pragma once
 #include "common.cuh"
 
 namespace bf {
 
+constexpr int pow2_floor(int x) { return x >= 32 ? 32 : x >= 16 ? 16 : x >= 8 ? 8 : x >= 4 ? 4 : x >= 2 ? 2 : 1; }
+
 template <int NP, int WW>
 struct RegCfg {
   static constexpr int np = NP, ww = WW;
   static constexpr int pairs = NP / 2;
-  static constexpr int chunks = (pairs + 15) / 16;  // 16 pairs per reduction chunk
   static constexpr int threads = 32 * WW;
-  static_assert(chunks <= 2, "at most 32 slot pairs (NP <= 64)");
+  static constexpr int rows = 32 * WW;
+  // slot-sum geometry: tpp threads per slot (power of two, one warp at most) each add rp rows
+  static constexpr int tpp = pow2_floor(rows / pairs);
+  static constexpr int rp = rows / tpp;
+  static constexpr int rs = rows + 2;  // product-buffer row stride (doubles; 16-byte multiple)
+  static_assert(pairs <= 32, "at most 32 slot pairs (NP <= 64)");
   static_assert(NP % 2 == 0 && NP >= 4, "even NP");
+  static_assert(rp % 4 == 0, "rows per slot part must be a multiple of 4");
 };
 
 // Named barrier among the WW row-warps of the CTA (id 1).
 BF_DEV void named_bar(int id, int nthreads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
-
-// Recursive-halving reduce of 16 values per lane: returns on every lane the full-warp sum
-// for pair index ((L>>4)&1)*8 + ((L>>3)&1)*4 + ((L>>2)&1)*2 + ((L>>1)&1).
-template <typename T>
-BF_DEV T halving16(T (&x)[16], int lane) {
-  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    T send = b4 ? x[i] : x[i + 8];
-    T keep = b4 ? x[i + 8] : x[i];
-    x[i] = keep + shfl_xor(send, 16);
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    T send = b3 ? x[i] : x[i + 4];
-    T keep = b3 ? x[i + 4] : x[i];
-    x[i] = keep + shfl_xor(send, 8);
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    T send = b2 ? x[i] : x[i + 2];
-    T keep = b2 ? x[i + 2] : x[i];
-    x[i] = keep + shfl_xor(send, 4);
-  }
-  T send = b1 ? x[0] : x[1];
-  T keep = b1 ? x[1] : x[0];
-  T v = keep + shfl_xor(send, 2);
-  return v + shfl_xor(v, 1);
-}
-
-BF_DEV int halving16_index(int lane) {
-  return ((lane >> 4) & 1) * 8 + ((lane >> 3) & 1) * 4 + ((lane >> 2) & 1) * 2 + ((lane >> 1) & 1);
-}
 
 // Rutishauser rotation returning t as well (jacobi.py:68-80), g_pq != 0.
 BF_DEV void jacobi_rotation_t(double gpp, double gpq, double gqq, double& c, double& s, double& t) {
@@ -146,7 +120,9 @@ struct RegGeom {
 #pragma unroll
     for (int k = 0; k < nslots<KIND>(); ++k) {
       const double2 p = *reinterpret_cast<const double2*>(cs + 2 * k);
-      if (p.y != 0.0) {
+      // round robin applies the identity to skipped pairs like the reference
+      // (jacobi.py:177-185); the serial sweep leaves them untouched (jacobi.py:134-136)
+      if (ORD == 1 || p.y != 0.0) {
         const T c = (T)p.x, sn = (T)p.y;
         T a = w[pa<KIND, PH>(k)], b = w[pb<KIND, PH>(k)];
         w[pa<KIND, PH>(k)] = fma(c, a, -sn * b);
@@ -243,76 +219,106 @@ struct RegDriver {
 };
 
 // ---------------------------------------------------------------------------------------------
+// CTA-level synchronisation among the WW row-warps (named barrier 1; a warp sync when WW == 1).
+template <int WW>
+BF_DEV void rows_sync() {
+  if (WW > 1)
+    named_bar(1, WW * 32);
+  else
+    __syncwarp();
+}
+// Barrier that also ORs a predicate over the WW*32 threads.
+template <int WW>
+BF_DEV int rows_sync_or(int pred) {
+  if (WW > 1) {
+    int r;
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\tsetp.ne.s32 p, %1, 0;\n\tbarrier.cta.red.or.pred q, 1, %2, p;\n\t"
+        "selp.s32 %0, 1, 0, q;\n\t}"
+        : "=r"(r)
+        : "r"(pred), "r"(WW * 32)
+        : "memory");
+    return r;
+  }
+  __syncwarp();
+  return __any_sync(FULL, pred);
+}
+
+// Sum of RP consecutive doubles in shared memory (16-byte aligned), four accumulators.
+template <int RP>
+BF_DEV double sum_rows(const double* p) {
+  static_assert(RP % 4 == 0, "RP multiple of 4");
+  const double2* q = reinterpret_cast<const double2*>(p);
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+#pragma unroll
+  for (int j = 0; j < RP / 4; ++j) {
+    const double2 x = q[2 * j], y = q[2 * j + 1];
+    a0 += x.x;
+    a1 += x.y;
+    a2 += y.x;
+    a3 += y.y;
+  }
+  return (a0 + a1) + (a2 + a3);
+}
+
 // W phase: sweeps until a rotation-free sweep (jacobi.py:270-281), logging (c, s) per slot.
-// Shared memory per warp: cs[32][2], d[NP] (tracked squared norms by column);
-// CTA-wide: red[WW][32] (cross-warp partials), red2[WW][64].
+// Per step: every row-thread writes its NS slot products w_a * w_b to the shared product
+// buffer P[slot][row] (one transposing store per slot, conflict-free); after one barrier,
+// TPP threads per slot sum RP rows each (vector loads) and combine by an xor butterfly, so
+// every one of them holds the same g_pq and computes the same rotation (no broadcast of the
+// scalars needed inside the slot group); one of them records (c, s) in cs[slot] and in the
+// log; after a second barrier (which also ORs the cancellation flags) every row applies all
+// slots. Column norms d[col] are tracked (dgesvj scheme, see header).
 template <typename T, class C, int ORD>
 struct WAction {
   using G = RegGeom<C, ORD>;
-  static constexpr int NP = C::np, NPAIR = C::pairs, WW = C::ww, CH = C::chunks;
+  static constexpr int NP = C::np, NPAIR = C::pairs, WW = C::ww;
+  static constexpr int TPP = C::tpp, RP = C::rp, RS = C::rs;
 
-  int lane, warp, n, max_sweeps;
+  int tid, n, max_sweeps;
   double tol2;
-  double* cs;    // this warp's (c, s) slot area, 32 x 2
-  double* d;     // this warp's tracked norms, NP
-  double* red;   // WW x 32
-  double* red2;  // WW x 64
+  double* cs;    // NPAIR x (c, s), CTA-shared
+  double* d;     // NP tracked squared norms by column, CTA-shared
+  double* P;     // 2 * NPAIR x RS product buffer, CTA-shared
+  int* swrot;    // 2 sweep rotation counters (parity), CTA-shared
   double2* log;  // this matrix's log cursor (global)
   int sweeps, conv, rot, recompute;
   long long rots;
 
-  // lane L computes pair k = chunk (L & 1) * 16 + halving16_index(L)
-  BF_DEV int my_pair() const { return (lane & 1) * 16 + halving16_index(lane); }
+  BF_DEV int slot() const { return tid / TPP; }
+  BF_DEV int part() const { return tid % TPP; }
+
+  BF_DEV double butterfly(double g) const {
+#pragma unroll
+    for (int o = TPP / 2; o > 0; o >>= 1) g += shfl_xor(g, o);
+    return g;
+  }
 
   // exact squared column norms of all NP positions (via the rr / odd-step slot pairing)
   template <int KIND, int PH>
   BF_DEV void norms(T (&w)[NP], int off, int t_rr) {
-    T na = T(0), nb = T(0);
 #pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      T x[16], y[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int k = c * 16 + i;
-        x[i] = y[i] = T(0);
-        if (k < NPAIR) {
-          T a = w[G::template pa<KIND, PH>(k)], b = w[G::template pb<KIND, PH>(k)];
-          x[i] = a * a;
-          y[i] = b * b;
-        }
-      }
-      T sx = halving16(x, lane), sy = halving16(y, lane);
-      if ((lane & 1) == c) {
-        na = sx;
-        nb = sy;
-      }
+    for (int k = 0; k < NPAIR; ++k) {
+      const T a = w[G::template pa<KIND, PH>(k)], b = w[G::template pb<KIND, PH>(k)];
+      P[k * RS + tid] = a * a;
+      P[(NPAIR + k) * RS + tid] = b * b;
     }
-    const int k = my_pair();
-    const bool mine = k < NPAIR;
-    double da = (double)na, db = (double)nb;
-    if (WW > 1) {
-      if (mine) {
-        red2[warp * 64 + 2 * k] = da;
-        red2[warp * 64 + 2 * k + 1] = db;
-      }
-      named_bar(1, WW * 32);
-      if (mine) {
-        da = db = 0.0;
-#pragma unroll
-        for (int q = 0; q < WW; ++q) {
-          da += red2[q * 64 + 2 * k];
-          db += red2[q * 64 + 2 * k + 1];
-        }
-      }
+    rows_sync<WW>();
+    const int k = slot(), h = part();
+    double da = 0.0, db = 0.0;
+    if (k < NPAIR) {
+      da = sum_rows<RP>(P + k * RS + h * RP);
+      db = sum_rows<RP>(P + (NPAIR + k) * RS + h * RP);
     }
-    if (mine) {
+    da = butterfly(da);
+    db = butterfly(db);
+    if (k < NPAIR && h == 0) {
       int ca, cb;
       G::template cols<KIND, PH>(k, t_rr, off, ca, cb);
       d[ca] = da;
       d[cb] = db;
     }
-    __syncwarp();
-    if (WW > 1) named_bar(1, WW * 32);  // red2 reuse
+    rows_sync<WW>();  // d visible, P free
     recompute = 0;
   }
 
@@ -332,68 +338,63 @@ struct WAction {
       norms<KIND == 0 ? 0 : 1, PH>(w, off, t_rr);
     }
     constexpr int NS = G::template nslots<KIND>();
-    T g = T(0);
 #pragma unroll
-    for (int c = 0; c < CH; ++c) {
-      T x[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int k = c * 16 + i;
-        x[i] = k < NS ? w[G::template pa<KIND, PH>(k)] * w[G::template pb<KIND, PH>(k)] : T(0);
-      }
-      T sg = halving16(x, lane);
-      if ((lane & 1) == c) g = sg;
-    }
-    const int k = my_pair();
-    const bool mine = k < NS;
-    double gpq = (double)g;
-    if (WW > 1) {
-      if (mine) red[warp * 32 + k] = gpq;
-      named_bar(1, WW * 32);
-      if (mine) {
-        gpq = 0.0;
-#pragma unroll
-        for (int q = 0; q < WW; ++q) gpq += red[q * 32 + k];
-      }
-    }
-    int flag = 0;
-    if (mine) {
+    for (int k = 0; k < NS; ++k) P[k * RS + tid] = w[G::template pa<KIND, PH>(k)] * w[G::template pb<KIND, PH>(k)];
+    rows_sync<WW>();
+    const int k = slot(), h = part();
+    double gpq = k < NS ? sum_rows<RP>(P + k * RS + h * RP) : 0.0;
+    gpq = butterfly(gpq);
+    int flag = 0, p = 0, q = 0;
+    bool did = false;
+    double cc = 1.0, sn = 0.0, np_ = 0.0, nq = 0.0;
+    if (k < NS) {
       int ca, cb;
       G::template cols<KIND, PH>(k, t_rr, off, ca, cb);
-      bool active = ORD == 1 || (ca != cb && ca < n && cb < n && ca + cb == s);
-      double cc = 1.0, sn = 0.0;
+      const bool active = ORD == 1 || (ca != cb && ca < n && cb < n && ca + cb == s);
       if (active) {
         const bool rev = ca > cb;  // slot a holds the larger column: rotate with swapped roles
-        const int p = rev ? cb : ca, q = rev ? ca : cb;
+        p = rev ? cb : ca;
+        q = rev ? ca : cb;
         const double dpp = d[p], dqq = d[q];
+        // skip rule (jacobi.py:134 / :167)
         if (gpq * gpq > tol2 * (dpp * dqq)) {
           double t;
           jacobi_rotation_t(dpp, gpq, dqq, cc, sn, t);
-          const double np_ = dpp - t * gpq, nq = dqq + t * gpq;
-          d[p] = np_ > 0.0 ? np_ : 0.0;
-          d[q] = nq > 0.0 ? nq : 0.0;
+          np_ = dpp - t * gpq;
+          nq = dqq + t * gpq;
           flag = (np_ < 1e-2 * dpp) | (nq < 1e-2 * dqq);  // cancellation -> recompute next step
           if (rev) sn = -sn;
-          ++rot;
+          did = true;
         }
       }
-      cs[2 * k] = cc;
-      cs[2 * k + 1] = sn;
     }
-    recompute = __any_sync(FULL, flag);
-    __syncwarp();
-    if (log != nullptr && warp == 0 && mine && (CH == 2 || (lane & 1) == 0)) log[k] = make_double2(cs[2 * k], cs[2 * k + 1]);
+    __syncwarp();  // every thread of the slot group has read d[p], d[q]
+    if (k < NS && h == 0) {
+      if (did) {
+        d[p] = np_ > 0.0 ? np_ : 0.0;
+        d[q] = nq > 0.0 ? nq : 0.0;
+        ++rot;
+      }
+      const double2 v = make_double2(cc, sn);
+      *reinterpret_cast<double2*>(cs + 2 * k) = v;
+      if (log != nullptr) log[k] = v;
+    }
     if (log != nullptr) log += NPAIR;
+    recompute = rows_sync_or<WW>(flag);
     G::template apply<T, KIND, PH>(w, cs);
-    __syncwarp();
   }
 
   BF_DEV bool sweep_end() {
-    // identical in every warp (identical sums and decisions); with one chunk each pair lives
-    // on two lanes, count it once
-    int r = (CH == 2 || (lane & 1) == 0) ? rot : 0;
+    int r = rot;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(FULL, r, o);
+    if (WW > 1) {
+      const int par = sweeps & 1;
+      if ((tid & 31) == 0) atomicAdd(swrot + par, r);
+      rows_sync<WW>();
+      r = swrot[par];
+      if (tid == 0) swrot[par ^ 1] = 0;
+    }
     rots += r;
     ++sweeps;
     if (r == 0) conv = 1;
@@ -401,33 +402,52 @@ struct WAction {
   }
 };
 
-// V phase: replay the logged rotations on V rows (lane = V row), staging the log through
-// shared memory STAGE steps at a time.
-template <typename T, class C, int ORD>
+// V phase: replay the logged rotations on V rows (lane = V row). The log streams through two
+// shared-memory stages of STAGE steps each: while one stage is replayed, cp.async fills the
+// other, so the (L2/DRAM-resident) log reads stay off the dependency chain.
+BF_DEV void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+BF_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+BF_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <typename T, class C, int ORD, int STAGE>
 struct VAction {
   using G = RegGeom<C, ORD>;
   static constexpr int NP = C::np, NPAIR = C::pairs, WW = C::ww;
-  static constexpr int STAGE = 8;
-  const double2* log;  // global cursor
-  double2* stage;      // STAGE x NPAIR smem (CTA-shared)
-  int in_stage, sweeps_left;
+  const double2* log;  // global cursor: next stage to prefetch
+  double2* stage;      // 2 x STAGE x NPAIR smem (CTA-shared)
+  int in_stage, cur, sweeps_left;
 
-  BF_DEV void refill() {
-    // all WW warps cooperatively copy the next STAGE steps (log is padded by STAGE steps)
-    if (WW > 1) named_bar(1, WW * 32);
-    __syncwarp();
-    for (int e = threadIdx.x; e < STAGE * NPAIR; e += WW * 32) stage[e] = log[e];
+  BF_DEV void prefetch(int buf) {
+    double2* dst = stage + buf * STAGE * NPAIR;
+    for (int e = threadIdx.x; e < STAGE * NPAIR; e += WW * 32) cp_async16(dst + e, log + e);
+    cp_async_commit();
     log += STAGE * NPAIR;
-    if (WW > 1) named_bar(1, WW * 32);
-    __syncwarp();
+  }
+  // all threads: stage 0 ready, stage 1 in flight (the log is padded by 2 STAGE steps)
+  BF_DEV void start() {
+    prefetch(0);
+    cp_async_wait_all();
+    prefetch(1);
+    rows_sync<WW>();
+    cur = 0;
+    in_stage = 0;
+  }
+  BF_DEV void next_stage() {
+    cp_async_wait_all();  // stage cur ^ 1 landed (this thread's part)
+    rows_sync<WW>();      // ... everyone's part, and everyone is done with stage cur
+    prefetch(cur);
+    cur ^= 1;
     in_stage = 0;
   }
   template <int PH>
   BF_DEV void sweep_start(T (&)[NP], int) {}
   template <int KIND, int PH>
   BF_DEV void step(T (&v)[NP], int, int, int) {
-    if (in_stage == STAGE) refill();
-    G::template apply<T, KIND, PH>(v, reinterpret_cast<const double*>(stage + in_stage * NPAIR));
+    if (in_stage == STAGE) next_stage();
+    G::template apply<T, KIND, PH>(v, reinterpret_cast<const double*>(stage + (cur * STAGE + in_stage) * NPAIR));
     ++in_stage;
   }
   BF_DEV bool sweep_end() { return --sweeps_left <= 0; }

@@ -40,14 +40,23 @@ constexpr int kStage = 8;
 
 template <class C>
 __host__ __device__ constexpr size_t reg_fixed_smem_doubles() {
-  // cs[WW][64] + d[WW][64] + red[WW][32] + red2[WW][64] + stage[kStage][32][2] + 8
-  return (size_t)C::ww * (64 + 64 + 32 + 64) + kStage * 64 + 8;
+  // cs[32][2] + d[64] + stage[2][kStage][32][2] + ctr[16 ints]
+  return 64 + 64 + 2 * kStage * 64 + 8;
+}
+
+// The work region holds the extraction arrays after the sweeps and the slot-product buffer
+// (2 * pairs x rs doubles) during them.
+template <class C>
+static size_t reg_work_bytes(int m, int nw, int es) {
+  size_t work = (size_t)m * nw > (size_t)nw * nw ? (size_t)m * nw : (size_t)nw * nw;
+  size_t ext = (work + 2 * (size_t)m + nw) * es + (size_t)nw * 4;
+  size_t prod = (size_t)2 * C::pairs * C::rs * 8;
+  return ext > prod ? ext : prod;
 }
 
 template <class C>
 static size_t reg_smem_bytes(int m, int nw, int es) {
-  size_t work = (size_t)m * nw > (size_t)nw * nw ? (size_t)m * nw : (size_t)nw * nw;
-  size_t b = reg_fixed_smem_doubles<C>() * 8 + (work + 2 * (size_t)m + nw) * es + (size_t)nw * 4 + 64;
+  size_t b = reg_fixed_smem_doubles<C>() * 8 + reg_work_bytes<C>(m, nw, es) + 64;
   return (b + 15) & ~(size_t)15;
 }
 
@@ -58,12 +67,10 @@ __global__ void __launch_bounds__(C::threads) svd_reg_kernel(RegArgs<T> a) {
   constexpr int NP = C::np, WW = C::ww;
   extern __shared__ __align__(16) double smem_d[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  double* cs_all = smem_d;
-  double* d_all = cs_all + WW * 64;
-  double* red = d_all + WW * 64;
-  double* red2 = red + WW * 32;
-  double2* stage = reinterpret_cast<double2*>(red2 + WW * 64);
-  int* ctr = reinterpret_cast<int*>(stage + kStage * 32);
+  double* cs_sh = smem_d;
+  double* d_sh = cs_sh + 64;
+  double2* stage = reinterpret_cast<double2*>(d_sh + 64);
+  int* ctr = reinterpret_cast<int*>(stage + 2 * kStage * 32);  // [0..8) extraction, [8..10) sweep counters
   T* Wsm = reinterpret_cast<T*>(smem_d + reg_fixed_smem_doubles<C>());
   const int m = a.m, n = a.n, nw = a.nw;
   const bool accv = a.v != nullptr;
@@ -85,21 +92,23 @@ __global__ void __launch_bounds__(C::threads) svd_reg_kernel(RegArgs<T> a) {
       if (row < m && col < n) val = a.ta ? A[(size_t)row * n + col] : A[(size_t)col * m + row];
       w[x] = val;
     }
+    if (tid == 0) ctr[8] = ctr[9] = 0;
+    __syncthreads();
     WAction<T, C, ORD> act;
-    act.lane = lane;
-    act.warp = warp;
+    act.tid = tid;
     act.n = n;
     act.max_sweeps = a.max_sweeps;
     act.tol2 = a.tol * a.tol;
-    act.cs = cs_all + warp * 64;
-    act.d = d_all + warp * 64;
-    act.red = red;
-    act.red2 = red2;
+    act.cs = cs_sh;
+    act.d = d_sh;
+    act.P = reinterpret_cast<double*>(Wsm);
+    act.swrot = ctr + 8;
     act.log = a.log ? a.log + (int64_t)blockIdx.x * a.log_stride : nullptr;
     act.sweeps = 0;
     act.conv = n < 2;
     act.rot = 0;
     act.recompute = 0;
+    static_assert(sizeof(T) == 8, "register tier is fp64");
     act.rots = 0;
     if (!act.conv) RegDriver<T, C, ORD>::run(w, n, act);
 
@@ -134,12 +143,13 @@ __global__ void __launch_bounds__(C::threads) svd_reg_kernel(RegArgs<T> a) {
         v[x] = col == row ? T(1) : T(0);
       }
       if (act.sweeps > 0) {
-        VAction<T, C, ORD> va;
+        VAction<T, C, ORD, kStage> va;
         va.log = a.log + (int64_t)blockIdx.x * a.log_stride;
         va.stage = stage;
-        va.in_stage = kStage;
         va.sweeps_left = act.sweeps;
+        va.start();
         RegDriver<T, C, ORD>::run(v, n, va);
+        cp_async_wait_all();  // the last prefetch (past the end of the log) must land before reuse
       }
       __syncthreads();  // everyone done with Wsm (extract) and the stage buffer
       if (row < nw) {
@@ -211,7 +221,7 @@ static int launch_reg(const SvdLaunch& L, void* ws, size_t ws_bytes, cudaStream_
   const int64_t cap = (int64_t)per_sm * sms;
   const int grid = (int)(L.batch < cap ? L.batch : cap);
   const int64_t log_stride =
-      ((int64_t)L.max_sweeps * reg_steps_per_sweep(C::np, L.n, ORD) + kStage + 1) * C::pairs;
+      ((int64_t)L.max_sweeps * reg_steps_per_sweep(C::np, L.n, ORD) + 2 * kStage + 1) * C::pairs;
   const size_t log_bytes = L.v ? (size_t)grid * log_stride * sizeof(double2) : 0;
   if (need) {
     *need = log_bytes;
