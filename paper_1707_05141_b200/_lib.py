@@ -9,7 +9,8 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbatchfact_b200.so")
+# BATCHFACT_B200_LIB overrides the library path (kernel experiments only)
+LIB_PATH = os.environ.get("BATCHFACT_B200_LIB") or os.path.join(HERE, "libbatchfact_b200.so")
 CSRC = os.path.join(HERE, "csrc")
 
 

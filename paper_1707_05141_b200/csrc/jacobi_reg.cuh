@@ -29,6 +29,16 @@
 
 namespace bf {
 
+#ifdef BF_PHASE_TIMING
+// kernel-experiment instrumentation: per-phase clock totals of warp 0 lane 0 (debug builds only)
+__device__ unsigned long long g_phase_clk[8];
+#define BF_T(i) long long _t##i = clock64()
+#define BF_ACC(slot, a, b) if (threadIdx.x == 0) atomicAdd(&g_phase_clk[slot], (unsigned long long)(_t##b - _t##a))
+#else
+#define BF_T(i)
+#define BF_ACC(slot, a, b)
+#endif
+
 constexpr int pow2_floor(int x) { return x >= 32 ? 32 : x >= 16 ? 16 : x >= 8 ? 8 : x >= 4 ? 4 : x >= 2 ? 2 : 1; }
 
 template <int NP, int WW>
@@ -338,12 +348,16 @@ struct WAction {
       norms<KIND == 0 ? 0 : 1, PH>(w, off, t_rr);
     }
     constexpr int NS = G::template nslots<KIND>();
+    BF_T(0);
 #pragma unroll
     for (int k = 0; k < NS; ++k) P[k * RS + tid] = w[G::template pa<KIND, PH>(k)] * w[G::template pb<KIND, PH>(k)];
+    BF_T(1);
     rows_sync<WW>();
+    BF_T(2);
     const int k = slot(), h = part();
     double gpq = k < NS ? sum_rows<RP>(P + k * RS + h * RP) : 0.0;
     gpq = butterfly(gpq);
+    BF_T(3);
     int flag = 0, p = 0, q = 0;
     bool did = false;
     double cc = 1.0, sn = 0.0, np_ = 0.0, nq = 0.0;
@@ -380,8 +394,18 @@ struct WAction {
       if (log != nullptr) log[k] = v;
     }
     if (log != nullptr) log += NPAIR;
+    BF_T(4);
     recompute = rows_sync_or<WW>(flag);
+    BF_T(5);
     G::template apply<T, KIND, PH>(w, cs);
+    BF_T(6);
+    BF_ACC(0, 0, 1);
+    BF_ACC(1, 1, 2);
+    BF_ACC(2, 2, 3);
+    BF_ACC(3, 3, 4);
+    BF_ACC(4, 4, 5);
+    BF_ACC(5, 5, 6);
+    BF_ACC(6, 0, 6);
   }
 
   BF_DEV bool sweep_end() {

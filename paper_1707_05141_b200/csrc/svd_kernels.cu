@@ -97,6 +97,7 @@ static int working_cols(int n, int ordering) { return (ordering == 1 && (n & 1))
 static bool fits_smem(size_t bytes) { return bytes <= 227 * 1024; }
 
 size_t svd_reg_ws_bytes(int dtype, const SvdLaunch& L);
+size_t svd_rr_ws_bytes(int dtype, const SvdLaunch& L);
 
 static size_t svd_shared_ws_bytes(int dtype, int64_t batch, int m, int n, int ordering, bool accv) {
   int nw = working_cols(n, ordering);
@@ -118,11 +119,14 @@ size_t svd_global_ws_bytes(int dtype, int64_t batch, int m, int n, int ordering,
   L.max_sweeps = max_sweeps;
   L.v = accv ? (void*)1 : nullptr;
   size_t r = svd_reg_ws_bytes(dtype, L);
+  const size_t rr = svd_rr_ws_bytes(dtype, L);
+  r = rr > r ? rr : r;
   size_t s = svd_shared_ws_bytes(dtype, batch, m, n, ordering, accv);
   return r > s ? r : s;
 }
 
 int launch_svd_reg(int dtype, const SvdLaunch& L, void* ws, size_t wsb, cudaStream_t st, bool* handled);
+int launch_svd_rr(int dtype, const SvdLaunch& L, void* ws, size_t wsb, cudaStream_t st, bool* handled);
 
 template <typename T>
 static int launch_svd_t(const SvdLaunch& L, void* ws, cudaStream_t st) {
@@ -167,7 +171,9 @@ int launch_svd(int dtype, const SvdLaunch& L, void* ws, size_t ws_bytes, cudaStr
   if (L.batch == 0) return 0;
   if (L.tier != 2) {
     bool handled = false;
-    int rc = launch_svd_reg(dtype, L, ws, ws_bytes, st, &handled);
+    int rc = launch_svd_rr(dtype, L, ws, ws_bytes, st, &handled);  // tiled round-robin register tier
+    if (handled || rc) return rc;
+    rc = launch_svd_reg(dtype, L, ws, ws_bytes, st, &handled);
     if (handled || rc) return rc;
   }
   return dtype == 0 ? launch_svd_t<double>(L, ws, st) : launch_svd_t<float>(L, ws, st);

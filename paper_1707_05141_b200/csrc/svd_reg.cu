@@ -63,7 +63,10 @@ static size_t reg_smem_bytes(int m, int nw, int es) {
 static int reg_steps_per_sweep(int np, int n, int ord) { return ord == 1 ? np - 1 : 2 * (n - 1); }
 
 template <typename T, class C, int ORD>
-__global__ void __launch_bounds__(C::threads) svd_reg_kernel(RegArgs<T> a) {
+#ifndef BF_REG_MINB
+#define BF_REG_MINB 1
+#endif
+__global__ void __launch_bounds__(C::threads, BF_REG_MINB) svd_reg_kernel(RegArgs<T> a) {
   constexpr int NP = C::np, WW = C::ww;
   extern __shared__ __align__(16) double smem_d[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -289,4 +292,14 @@ int launch_svd_reg(int dtype, const SvdLaunch& L, void* ws, size_t wsb, cudaStre
   return rc;
 }
 
+#ifdef BF_PHASE_TIMING
+extern "C" __attribute__((visibility("default"))) int bf_debug_phase_clk(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, g_phase_clk, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_phase_clk, z, sizeof(z));
+  }
+  return (int)cudaGetLastError();
+}
+#endif
 }  // namespace bf

@@ -1,0 +1,613 @@
+// Tiled register tier of the batched one-sided Jacobi SVD, round-robin ordering.
+//
+// Reference: _round_robin_sweep jacobi.py:158-186 (skip rule :167, identity for skipped pairs
+// :177-185), svd :231-284 (sweep until a rotation-free sweep :270-281, off_orthogonality
+// fallback :282-283, _extract_svd :212-228), round_robin_schedule :102-115.
+//
+// Layout. The round-robin schedule pairs positions (k, NP-1-k) (slot k) and after every step
+// moves positions 1..NP-1 one place on (idx = [idx0, idx[-1]] + idx[1:-1]). A thread owns an
+// R-row x S-slot tile of W: for each of its rows the S "a" positions sg*S + j and the S "b"
+// positions NP-1-(sg*S + j) of slot group sg. Lane = rgl * SG + sg (rgl = row group within the
+// warp), so the SG slot groups of a row group are adjacent lanes:
+//   * a step's data movement is a FIFO shift inside each thread (compile-time register renaming
+//     with period S, no moves) plus ONE value per row and direction crossing to the neighbouring
+//     slot group (shfl up/down within SG lanes); the fixed position 0 and the ring's turn at the
+//     middle are two per-lane selects;
+//   * g_pq is a per-thread R-row partial, a shuffle butterfly over the warp's row groups and, for
+//     NWARP > 1, one shared-memory exchange between warps (the only barrier of a step);
+//   * lane rgl == j of each slot group computes slot j's Rutishauser rotation
+//     (jacobi.py:68-80) -- every warp redundantly, on identical inputs -- and the S (c, s) pairs
+//     reach the group's lanes by shuffles.
+// Shared-memory traffic per step is a few hundred bytes per matrix (the row-per-thread layout
+// of svd_reg.cu moves ~64 KB through shared memory per 64 x 64 step).
+// Column norms are tracked (dgesvj scheme, see jacobi_reg.cuh) and recomputed at sweep start
+// and after cancellation. V is rebuilt from a rotation log replayed on the same tiles.
+#include "internal.h"
+#include "jacobi_cta.cuh"
+#include "jacobi_reg.cuh"
+
+namespace bf {
+
+template <int NP_, int S_, int R_, int NW_>
+struct RRCfg {
+  static constexpr int NP = NP_, S = S_, R = R_, NWARP = NW_;
+  static constexpr int NPAIR = NP / 2;
+  static constexpr int SG = NPAIR / S;     // slot groups
+  static constexpr int RGW = 32 / SG;      // row groups per warp
+  static constexpr int ROWS = RGW * NWARP * R;
+  static constexpr int THREADS = 32 * NWARP;
+  static_assert(NPAIR % S == 0, "S divides the pair count");
+  static_assert(32 % SG == 0 && SG >= 2, "slot groups tile a warp");
+  static_assert(RGW >= S, "one rotation lane per slot in every slot group");
+};
+
+#ifndef BF_RR_STAGE
+#define BF_RR_STAGE 8
+#endif
+constexpr int kRRStage = BF_RR_STAGE;
+
+#ifndef BF_RR64_R
+#define BF_RR64_R 8  // rows per thread for 64 x 64 (8 -> 2 warps, 4 -> 4 warps per matrix)
+#endif
+
+template <typename C>
+struct RRShared {
+  // carved out of the extraction work region (free during the sweeps)
+  static constexpr int PART = 2 * C::NWARP * 2 * C::NPAIR;  // [parity][warp][2 * NPAIR]
+  static constexpr int DN = C::NWARP * C::NP;               // tracked norms per warp
+  static constexpr int STAGE = 2 * kRRStage * C::NPAIR * 2; // V log staging (doubles)
+  static constexpr int SWEEP = PART + DN;
+};
+
+BF_DEV void rr_bar(int nthreads) { asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory"); }
+
+// column held by position x at round-robin step t (jacobi.py:111-114)
+template <int NP>
+BF_DEV int rr_col(int x, int t) {
+  if (x == 0) return 0;
+  int v = x - 1 - t;
+  v += v < 0 ? NP - 1 : 0;
+  return 1 + v;
+}
+
+template <class C>
+struct RRTile {
+  static constexpr int S = C::S, R = C::R, SG = C::SG;
+  double A[R][S], B[R][S];  // physical FIFO registers
+
+  // logical a[j] / b[j] at phase PH
+  template <int PH>
+  static BF_DEV constexpr int ia(int j) {
+    return ((j - PH) % S + S) % S;
+  }
+  template <int PH>
+  static BF_DEV constexpr int ib(int j) {
+    return (j + PH) % S;
+  }
+
+  template <int PH>
+  BF_DEV void apply(const double (&c)[S], const double (&s)[S]) {
+#pragma unroll
+    for (int j = 0; j < S; ++j)
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const double a = A[i][ia<PH>(j)], b = B[i][ib<PH>(j)];
+        A[i][ia<PH>(j)] = fma(c[j], a, -s[j] * b);
+        B[i][ib<PH>(j)] = fma(s[j], a, c[j] * b);
+      }
+  }
+
+  // one round-robin move: positions 1..NP-1 advance one place; the tile goes from phase PH to PH+1
+  template <int PH>
+  BF_DEV void move(int sg) {
+    constexpr int XA = ia<PH>(S - 1);  // exiting a register -> logical a[0] at PH+1
+    constexpr int YA = ia<PH>(0);      // old a[0] -> logical a[1] at PH+1
+    constexpr int XB = ib<PH>(0);      // exiting b register -> logical b[S-1] at PH+1
+    const bool first = sg == 0, last = sg == SG - 1;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const double a_exit = A[i][XA], b_exit = B[i][XB];
+      const double ra = __shfl_up_sync(FULL, a_exit, 1, SG);
+      const double rb = __shfl_down_sync(FULL, b_exit, 1, SG);
+      // slot group 0: position 0 is fixed and position 1 takes position NP-1's value
+      const double y = A[i][YA];
+      A[i][XA] = first ? y : ra;
+      A[i][YA] = first ? b_exit : y;
+      // last slot group: the ring turns from position NP/2-1 to NP/2 inside the thread
+      B[i][XB] = last ? a_exit : rb;
+    }
+  }
+
+  template <int PH>
+  BF_DEV void partial_dots(double (&g)[S]) const {
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      double acc = A[0][ia<PH>(j)] * B[0][ib<PH>(j)];
+#pragma unroll
+      for (int i = 1; i < R; ++i) acc = fma(A[i][ia<PH>(j)], B[i][ib<PH>(j)], acc);
+      g[j] = acc;
+    }
+  }
+  template <int PH>
+  BF_DEV void partial_norms(double (&na)[S], double (&nb)[S]) const {
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      double xa = A[0][ia<PH>(j)] * A[0][ia<PH>(j)], xb = B[0][ib<PH>(j)] * B[0][ib<PH>(j)];
+#pragma unroll
+      for (int i = 1; i < R; ++i) {
+        xa = fma(A[i][ia<PH>(j)], A[i][ia<PH>(j)], xa);
+        xb = fma(B[i][ib<PH>(j)], B[i][ib<PH>(j)], xb);
+      }
+      na[j] = xa;
+      nb[j] = xb;
+    }
+  }
+
+  // positions -> columns at t == 0 (identity): write the tile to column-major smem (ld rows)
+  template <int PH>
+  BF_DEV void store(double* M, int ld, int nrows, int ncols, int row0, int sg) const {
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const int ca = sg * S + j, cb = C::NP - 1 - (sg * S + j);
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int r = row0 + i;
+        if (r < nrows) {
+          if (ca < ncols) M[(size_t)ca * ld + r] = A[i][ia<PH>(j)];
+          if (cb < ncols) M[(size_t)cb * ld + r] = B[i][ib<PH>(j)];
+        }
+      }
+    }
+  }
+  BF_DEV void store_phase(int ph, double* M, int ld, int nrows, int ncols, int row0, int sg) const {
+    switch (ph) {
+      case 0: store<0>(M, ld, nrows, ncols, row0, sg); break;
+      case 1: store<1 % S>(M, ld, nrows, ncols, row0, sg); break;
+      case 2: store<2 % S>(M, ld, nrows, ncols, row0, sg); break;
+      case 3: store<3 % S>(M, ld, nrows, ncols, row0, sg); break;
+      case 4: store<4 % S>(M, ld, nrows, ncols, row0, sg); break;
+      default: store<5 % S>(M, ld, nrows, ncols, row0, sg); break;
+    }
+  }
+};
+
+// lane-dependent pick of x[j] for j = idx (idx < S), uniform code
+template <int S>
+BF_DEV double pick(const double (&x)[S], int idx) {
+  double r = x[0];
+#pragma unroll
+  for (int j = 1; j < S; ++j) r = idx == j ? x[j] : r;
+  return r;
+}
+
+template <class C>
+struct RRWork {
+  static constexpr int S = C::S, SG = C::SG, NP = C::NP, NPAIR = C::NPAIR, NWARP = C::NWARP;
+  int lane, warp, sg, rgl, n, max_sweeps;
+  double tol2;
+  double* part;  // [2][NWARP][2 * NPAIR]
+  double* d;     // this warp's NP tracked norms
+  double2* log;  // global cursor (warp 0 writes)
+  int ex, sweeps, conv, rot, recompute;
+  long long rots;
+
+  BF_DEV bool rot_lane() const { return rgl < S; }
+  BF_DEV int slot() const { return sg * S + rgl; }
+
+  // sum over the warp's row groups (xor over the lane bits above the slot-group bits)
+  template <int K>
+  BF_DEV void warp_sum(double (&x)[K]) const {
+#pragma unroll
+    for (int o = SG; o < 32; o <<= 1)
+#pragma unroll
+      for (int j = 0; j < K; ++j) x[j] += __shfl_xor_sync(FULL, x[j], o);
+  }
+  // add the other warps' partials of this lane's slot value(s) (fixed warp order)
+  template <int K>
+  BF_DEV void cross_warp(double (&v)[K]) {
+    if (NWARP == 1) return;
+    double* buf = part + (ex & 1) * NWARP * 2 * NPAIR;
+    ++ex;
+    if (rot_lane())
+#pragma unroll
+      for (int q = 0; q < K; ++q) buf[warp * 2 * NPAIR + q * NPAIR + slot()] = v[q];
+    rr_bar(C::THREADS);
+    if (rot_lane()) {
+#pragma unroll
+      for (int q = 0; q < K; ++q) {
+        double tot = buf[q * NPAIR + slot()];
+#pragma unroll
+        for (int w = 1; w < NWARP; ++w) tot += buf[w * 2 * NPAIR + q * NPAIR + slot()];
+        v[q] = tot;
+      }
+    }
+  }
+
+  template <int PH>
+  BF_DEV void norms(RRTile<C>& tile, int t) {
+    double na[S], nb[S];
+    tile.template partial_norms<PH>(na, nb);
+    warp_sum(na);
+    warp_sum(nb);
+    double v[2] = {pick<S>(na, rgl), pick<S>(nb, rgl)};
+    cross_warp(v);
+    if (rot_lane()) {
+      const int k = slot();
+      d[rr_col<NP>(k, t)] = v[0];
+      d[rr_col<NP>(NP - 1 - k, t)] = v[1];
+    }
+    __syncwarp();
+    recompute = 0;
+  }
+
+  template <int PH>
+  BF_DEV void sweep_start(RRTile<C>& tile, int t) {
+    rot = 0;
+    norms<PH>(tile, t);
+  }
+
+  template <int PH>
+  BF_DEV void step(RRTile<C>& tile, int t) {
+    if (recompute) norms<PH>(tile, t);
+    double g[S];
+    tile.template partial_dots<PH>(g);
+    warp_sum(g);
+    double v[1] = {pick<S>(g, rgl)};
+    cross_warp(v);
+    double cc = 1.0, sn = 0.0;
+    int flag = 0;
+    if (rot_lane()) {
+      const int k = slot();
+      const int ca = rr_col<NP>(k, t), cb = rr_col<NP>(NP - 1 - k, t);
+      const bool rev = ca > cb;  // slot a holds the larger column: rotate with swapped roles
+      const int p = rev ? cb : ca, q = rev ? ca : cb;
+      const double dpp = d[p], dqq = d[q], gpq = v[0];
+      if (gpq * gpq > tol2 * (dpp * dqq)) {  // skip rule (jacobi.py:167)
+        double tt;
+        jacobi_rotation_t(dpp, gpq, dqq, cc, sn, tt);
+        const double np_ = dpp - tt * gpq, nq = dqq + tt * gpq;
+        d[p] = np_ > 0.0 ? np_ : 0.0;
+        d[q] = nq > 0.0 ? nq : 0.0;
+        flag = (np_ < 1e-2 * dpp) | (nq < 1e-2 * dqq);  // cancellation -> recompute next step
+        if (rev) sn = -sn;
+        ++rot;
+      }
+      if (log != nullptr && warp == 0) log[k] = make_double2(cc, sn);
+    }
+    if (log != nullptr) log += NPAIR;
+    recompute = __any_sync(FULL, flag);
+    double c[S], s[S];
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      c[j] = __shfl_sync(FULL, cc, j * SG + sg);
+      s[j] = __shfl_sync(FULL, sn, j * SG + sg);
+    }
+    tile.template apply<PH>(c, s);
+    tile.template move<PH>(sg);
+  }
+
+  BF_DEV bool sweep_end() {
+    const int r = __reduce_add_sync(FULL, rot);  // identical in every warp
+    rots += r;
+    ++sweeps;
+    if (r == 0) conv = 1;
+    return conv || sweeps >= max_sweeps;
+  }
+};
+
+template <class C>
+struct RRReplay {
+  static constexpr int S = C::S, SG = C::SG, NPAIR = C::NPAIR;
+  const double2* log;  // global cursor: next stage to prefetch
+  double2* stage;      // 2 x kRRStage x NPAIR
+  int sg, in_stage, cur, sweeps_left;
+
+  BF_DEV void prefetch(int buf) {
+    double2* dst = stage + buf * kRRStage * NPAIR;
+    for (int e = threadIdx.x; e < kRRStage * NPAIR; e += C::THREADS) cp_async16(dst + e, log + e);
+    cp_async_commit();
+    log += kRRStage * NPAIR;
+  }
+  BF_DEV void start() {
+    prefetch(0);
+    cp_async_wait_all();
+    prefetch(1);
+    __syncthreads();
+    cur = 0;
+    in_stage = 0;
+  }
+  template <int PH>
+  BF_DEV void sweep_start(RRTile<C>&, int) {}
+  template <int PH>
+  BF_DEV void step(RRTile<C>& tile, int) {
+    if (in_stage == kRRStage) {
+      cp_async_wait_all();
+      __syncthreads();
+      prefetch(cur);
+      cur ^= 1;
+      in_stage = 0;
+    }
+    const double2* e = stage + (cur * kRRStage + in_stage) * NPAIR + sg * S;
+    double c[S], s[S];
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const double2 x = e[j];
+      c[j] = x.x;
+      s[j] = x.y;
+    }
+    ++in_stage;
+    tile.template apply<PH>(c, s);
+    tile.template move<PH>(sg);
+  }
+  BF_DEV bool sweep_end() { return --sweeps_left <= 0; }
+};
+
+// Drives sweeps of NP-1 steps through the S-periodic register phases; returns the final phase.
+template <class C, class Act>
+struct RRDriver {
+  static constexpr int S = C::S, NP = C::NP;
+  template <int PH>
+  static BF_DEV bool at(RRTile<C>& tile, Act& act, int& t) {
+    act.template step<PH>(tile, t);
+    if (++t == NP - 1) {
+      t = 0;
+      if (act.sweep_end()) return true;
+      act.template sweep_start<(PH + 1) % S>(tile, 0);
+    }
+    return false;
+  }
+  static BF_DEV int run(RRTile<C>& tile, Act& act) {
+    int t = 0;
+    act.template sweep_start<0>(tile, 0);
+    for (;;) {
+      if (at<0>(tile, act, t)) return 1 % S;
+      if (at<1 % S>(tile, act, t)) return 2 % S;
+      if (at<2 % S>(tile, act, t)) return 3 % S;
+      if (at<3 % S>(tile, act, t)) return 4 % S;
+      if constexpr (S > 4)
+        if (at<4 % S>(tile, act, t)) return 5 % S;
+      if constexpr (S > 5)
+        if (at<5 % S>(tile, act, t)) return 6 % S;
+    }
+  }
+};
+
+template <typename T>
+struct RRArgs {
+  int64_t batch;
+  int m, n, nw;
+  const T* a;
+  int64_t a_stride;
+  bool ta;
+  T* u;
+  int64_t u_stride;
+  T* s;
+  int64_t s_stride;
+  T* v;
+  int64_t v_stride;
+  int32_t* sweeps;
+  uint8_t* conv;
+  int64_t* rots;
+  double tol;
+  int max_sweeps;
+  double2* log;
+  int64_t log_stride;
+  const uint8_t* active;
+};
+
+// work region (extraction arrays; the sweep buffers and the V log stage alias its start)
+template <class C>
+__host__ __device__ static size_t rr_region_doubles(int m, int nw) {
+  size_t r = (size_t)m * nw > (size_t)nw * nw ? (size_t)m * nw : (size_t)nw * nw;
+  if ((size_t)RRShared<C>::SWEEP > r) r = RRShared<C>::SWEEP;
+  if ((size_t)RRShared<C>::STAGE > r) r = RRShared<C>::STAGE;
+  return r;
+}
+
+template <class C>
+static size_t rr_smem_bytes(int m, int nw) {
+  const size_t d = 8 + rr_region_doubles<C>(m, nw) + 2 * (size_t)m + nw + ((size_t)nw * 4 + 7) / 8;
+  return (d * 8 + 15) & ~(size_t)15;
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS) svd_rr_kernel(RRArgs<double> a) {
+  extern __shared__ __align__(16) double sm[];
+  int* ctr = reinterpret_cast<int*>(sm);  // 16 ints: extraction counters
+  double* Wsm = sm + 8;
+  const int m = a.m, n = a.n, nw = a.nw;
+  double* cand = Wsm + rr_region_doubles<C>(m, nw);
+  double* sig = cand + 2 * m;
+  int* order = reinterpret_cast<int*>(sig + nw);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int sg = lane % C::SG, rgl = lane / C::SG;
+  const int row0 = (warp * C::RGW + rgl) * C::R;
+  const bool accv = a.v != nullptr;
+
+  for (int64_t b = blockIdx.x; b < a.batch; b += gridDim.x) {
+    if (a.active && !a.active[b]) continue;  // uniform across the CTA
+    const double* Ab = a.a + b * a.a_stride;
+    RRTile<C> tile;
+#pragma unroll
+    for (int j = 0; j < C::S; ++j) {
+      const int ca = sg * C::S + j, cb = C::NP - 1 - (sg * C::S + j);
+#pragma unroll
+      for (int i = 0; i < C::R; ++i) {
+        const int r = row0 + i;
+        double xa = 0.0, xb = 0.0;
+        if (r < m) {
+          if (ca < n) xa = a.ta ? Ab[(size_t)r * n + ca] : Ab[(size_t)ca * m + r];
+          if (cb < n) xb = a.ta ? Ab[(size_t)r * n + cb] : Ab[(size_t)cb * m + r];
+        }
+        tile.A[i][j] = xa;  // phase 0: logical == physical
+        tile.B[i][j] = xb;
+      }
+    }
+    RRWork<C> wk;
+    wk.lane = lane;
+    wk.warp = warp;
+    wk.sg = sg;
+    wk.rgl = rgl;
+    wk.n = n;
+    wk.max_sweeps = a.max_sweeps;
+    wk.tol2 = a.tol * a.tol;
+    wk.part = Wsm;
+    wk.d = Wsm + RRShared<C>::PART + warp * C::NP;
+    wk.log = a.log ? a.log + (int64_t)blockIdx.x * a.log_stride : nullptr;
+    wk.ex = 0;
+    wk.sweeps = 0;
+    wk.conv = n < 2;
+    wk.rot = 0;
+    wk.recompute = 0;
+    wk.rots = 0;
+    __syncthreads();  // previous matrix done with the shared region
+    int ph = 0;
+    if (!wk.conv) ph = RRDriver<C, RRWork<C>>::run(tile, wk);
+
+    // ---- W -> shared memory (column-major m x nw), off-orthogonality fallback, extraction
+    __syncthreads();
+    tile.store_phase(ph, Wsm, m, m, nw, row0, sg);
+    __syncthreads();
+    int conv = wk.conv;
+    if (!conv) {  // jacobi.py:282-283
+      double off = off_orthogonality_cta<double>(Wsm, m, m, nw, sig, reinterpret_cast<double*>(ctr + 2));
+      conv = off < a.tol;
+    }
+    extract_svd_cta<double>(Wsm, m, nullptr, nw, m, n, n, 0, a.u + b * a.u_stride, m, a.s + b * a.s_stride, nullptr, n,
+                            sig, order, cand, ctr + 6);
+    if (tid == 0) {
+      if (a.sweeps) a.sweeps[b] = wk.sweeps;
+      if (a.conv) a.conv[b] = (uint8_t)conv;
+      if (a.rots) a.rots[b] = wk.rots;
+    }
+    if (accv) {
+      // ---- V: identity, replay the log on the same tiles, write in sorted order
+#pragma unroll
+      for (int j = 0; j < C::S; ++j) {
+        const int ca = sg * C::S + j, cb = C::NP - 1 - (sg * C::S + j);
+#pragma unroll
+        for (int i = 0; i < C::R; ++i) {
+          tile.A[i][j] = (row0 + i == ca) ? 1.0 : 0.0;
+          tile.B[i][j] = (row0 + i == cb) ? 1.0 : 0.0;
+        }
+      }
+      int vph = 0;
+      __syncthreads();  // extraction done with the work region (stage lives there)
+      if (wk.sweeps > 0) {
+        RRReplay<C> rp;
+        rp.log = a.log + (int64_t)blockIdx.x * a.log_stride;
+        rp.stage = reinterpret_cast<double2*>(Wsm);
+        rp.sg = sg;
+        rp.sweeps_left = wk.sweeps;
+        rp.start();
+        vph = RRDriver<C, RRReplay<C>>::run(tile, rp);
+        cp_async_wait_all();
+      }
+      __syncthreads();
+      tile.store_phase(vph, Wsm, nw, nw, nw, row0, sg);
+      __syncthreads();
+      double* Vo = a.v + b * a.v_stride;
+      for (int e = tid; e < n * n; e += blockDim.x) {
+        const int r = e / n, i = e % n;
+        Vo[(size_t)r * n + i] = Wsm[(size_t)order[r] * nw + i];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------------------ dispatch
+
+template <class C>
+static int launch_rr(const SvdLaunch& L, int nw, void* ws, size_t ws_bytes, cudaStream_t st, size_t* need) {
+  const size_t smem = rr_smem_bytes<C>(L.m, nw);
+  if (smem > 227 * 1024) return -1;
+  cudaError_t e = cudaFuncSetAttribute(svd_rr_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return (int)e;
+  int per_sm = 0, dev = 0, sms = 148;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, svd_rr_kernel<C>, C::THREADS, smem);
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t cap = (int64_t)per_sm * sms;
+  const int grid = (int)(L.batch < cap ? L.batch : cap);
+  // the replay prefetches up to two stages past the last logged step
+  const int64_t log_stride = ((int64_t)L.max_sweeps * (C::NP - 1) + 2 * kRRStage + 1) * C::NPAIR;
+  const size_t log_bytes = L.v ? (size_t)grid * log_stride * sizeof(double2) : 0;
+  if (need) {
+    *need = log_bytes;
+    return 0;
+  }
+  if (log_bytes && (!ws || ws_bytes < log_bytes)) return -2;
+  RRArgs<double> a;
+  a.batch = L.batch;
+  a.m = L.m;
+  a.n = L.n;
+  a.nw = nw;
+  a.a = (const double*)L.a;
+  a.a_stride = L.a_stride;
+  a.ta = L.transpose_a;
+  a.u = (double*)L.u;
+  a.u_stride = L.u_stride;
+  a.s = (double*)L.s;
+  a.s_stride = L.s_stride;
+  a.v = (double*)L.v;
+  a.v_stride = L.v_stride;
+  a.sweeps = L.sweeps;
+  a.conv = L.converged;
+  a.rots = L.rotations;
+  a.tol = L.tol;
+  a.max_sweeps = L.max_sweeps;
+  a.log = L.v ? (double2*)ws : nullptr;
+  a.log_stride = log_stride;
+  a.active = L.active;
+  svd_rr_kernel<C><<<grid, C::THREADS, smem, st>>>(a);
+  return (int)cudaGetLastError();
+}
+
+// -1: shape not covered by an instantiation
+static int rr_dispatch(const SvdLaunch& L, void* ws, size_t wsb, cudaStream_t st, size_t* need) {
+  const int nw = (L.n & 1) ? L.n + 1 : L.n;
+  const int rows = L.m > nw ? L.m : nw;
+  switch (nw) {
+    case 16:
+      if (rows <= 16) return launch_rr<RRCfg<16, 4, 1, 1>>(L, nw, ws, wsb, st, need);
+      if (rows <= 32) return launch_rr<RRCfg<16, 4, 2, 1>>(L, nw, ws, wsb, st, need);
+      if (rows <= 64) return launch_rr<RRCfg<16, 4, 4, 1>>(L, nw, ws, wsb, st, need);
+      return -1;
+    case 32:
+      if (rows <= 32) return launch_rr<RRCfg<32, 4, 4, 1>>(L, nw, ws, wsb, st, need);
+      if (rows <= 64) return launch_rr<RRCfg<32, 4, 4, 2>>(L, nw, ws, wsb, st, need);
+      return -1;
+    case 40:
+      if (rows <= 40) return launch_rr<RRCfg<40, 5, 5, 1>>(L, nw, ws, wsb, st, need);
+      if (rows <= 64) return launch_rr<RRCfg<40, 5, 4, 2>>(L, nw, ws, wsb, st, need);
+      return -1;
+    case 48:
+      if (rows <= 48) return launch_rr<RRCfg<48, 6, 3, 2>>(L, nw, ws, wsb, st, need);
+      if (rows <= 64) return launch_rr<RRCfg<48, 6, 4, 2>>(L, nw, ws, wsb, st, need);
+      return -1;
+    case 64:
+      if (rows <= 64) return launch_rr<RRCfg<64, 4, BF_RR64_R, 64 / (4 * BF_RR64_R)>>(L, nw, ws, wsb, st, need);
+      return -1;
+    default:
+      return -1;
+  }
+}
+
+size_t svd_rr_ws_bytes(int dtype, const SvdLaunch& L) {
+  if (dtype != 0 || L.ordering != 1 || L.tier == 2 || L.n < 2) return 0;
+  size_t need = 0;
+  return rr_dispatch(L, nullptr, 0, nullptr, &need) == 0 ? need : 0;
+}
+
+int launch_svd_rr(int dtype, const SvdLaunch& L, void* ws, size_t wsb, cudaStream_t st, bool* handled) {
+  *handled = false;
+  if (dtype != 0 || L.ordering != 1 || L.tier == 2 || L.n < 2) return 0;
+  const int rc = rr_dispatch(L, ws, wsb, st, nullptr);
+  if (rc == -1 || rc == -2) return 0;
+  *handled = true;
+  return rc;
+}
+
+}  // namespace bf
