@@ -73,7 +73,8 @@ BF_DEV int rr_col(int x, int t) {
 template <class C>
 struct RRTile {
   static constexpr int S = C::S, R = C::R, SG = C::SG;
-  double A[R][S], B[R][S];  // physical FIFO registers
+  double A[R][S], B[R][S];  // physical FIFO registers (scaled columns: true = stored * scale)
+  double FA[S], FB[S];      // per-position column scales of this slot group (W phase)
 
   // logical a[j] / b[j] at phase PH
   template <int PH>
@@ -85,37 +86,83 @@ struct RRTile {
     return (j + PH) % S;
   }
 
+  // Scaled rotation (the deferred-normalisation form of the rotation, cf. LAPACK dgesvj's
+  // fast rotations): with true columns a = fa * ~a, b = fb * ~b the rotation
+  // a' = c a - s b, b' = s a + c b is ~a' = ~a + al ~b, ~b' = ~b + be ~a with
+  // al = -t fb / fa, be = t fa / fb and the scales multiplied by c -- 2 FMAs per element
+  // instead of 2 multiplies + 2 FMAs. Skipped pairs have al = be = 0.
   template <int PH>
-  BF_DEV void apply(const double (&c)[S], const double (&s)[S]) {
+  BF_DEV void apply(const double (&al)[S], const double (&be)[S]) {
 #pragma unroll
     for (int j = 0; j < S; ++j)
 #pragma unroll
       for (int i = 0; i < R; ++i) {
         const double a = A[i][ia<PH>(j)], b = B[i][ib<PH>(j)];
-        A[i][ia<PH>(j)] = fma(c[j], a, -s[j] * b);
-        B[i][ib<PH>(j)] = fma(s[j], a, c[j] * b);
+        A[i][ia<PH>(j)] = fma(al[j], b, a);
+        B[i][ib<PH>(j)] = fma(be[j], a, b);
       }
+  }
+  template <int PH>
+  BF_DEV void scale_update(const double (&c)[S]) {
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      FA[ia<PH>(j)] *= c[j];
+      FB[ib<PH>(j)] *= c[j];
+    }
+  }
+  // fold the scales into the columns (phase independent: physical registers pair up)
+  BF_DEV void renormalize() {
+#pragma unroll
+    for (int x = 0; x < S; ++x) {
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        A[i][x] *= FA[x];
+        B[i][x] *= FB[x];
+      }
+      FA[x] = 1.0;
+      FB[x] = 1.0;
+    }
+  }
+  BF_DEV void unit_scales() {
+#pragma unroll
+    for (int x = 0; x < S; ++x) FA[x] = FB[x] = 1.0;
+  }
+  // multiply columns by per-column factors (t == 0: position == column), phase PH
+  template <int PH>
+  BF_DEV void scale_cols(const double* f, int sg) {
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const double fa = f[sg * S + j], fb = f[C::NP - 1 - (sg * S + j)];
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        A[i][ia<PH>(j)] *= fa;
+        B[i][ib<PH>(j)] *= fb;
+      }
+    }
   }
 
   // one round-robin move: positions 1..NP-1 advance one place; the tile goes from phase PH to PH+1
   template <int PH>
-  BF_DEV void move(int sg) {
+  static BF_DEV void move1(double (&a)[S], double (&b)[S], bool first, bool last) {
     constexpr int XA = ia<PH>(S - 1);  // exiting a register -> logical a[0] at PH+1
     constexpr int YA = ia<PH>(0);      // old a[0] -> logical a[1] at PH+1
     constexpr int XB = ib<PH>(0);      // exiting b register -> logical b[S-1] at PH+1
+    const double a_exit = a[XA], b_exit = b[XB];
+    const double ra = __shfl_up_sync(FULL, a_exit, 1, SG);
+    const double rb = __shfl_down_sync(FULL, b_exit, 1, SG);
+    // slot group 0: position 0 is fixed and position 1 takes position NP-1's value
+    const double y = a[YA];
+    a[XA] = first ? y : ra;
+    a[YA] = first ? b_exit : y;
+    // last slot group: the ring turns from position NP/2-1 to NP/2 inside the thread
+    b[XB] = last ? a_exit : rb;
+  }
+  template <int PH, bool SCALES>
+  BF_DEV void move(int sg) {
     const bool first = sg == 0, last = sg == SG - 1;
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
-      const double a_exit = A[i][XA], b_exit = B[i][XB];
-      const double ra = __shfl_up_sync(FULL, a_exit, 1, SG);
-      const double rb = __shfl_down_sync(FULL, b_exit, 1, SG);
-      // slot group 0: position 0 is fixed and position 1 takes position NP-1's value
-      const double y = A[i][YA];
-      A[i][XA] = first ? y : ra;
-      A[i][YA] = first ? b_exit : y;
-      // last slot group: the ring turns from position NP/2-1 to NP/2 inside the thread
-      B[i][XB] = last ? a_exit : rb;
-    }
+    for (int i = 0; i < R; ++i) move1<PH>(A[i], B[i], first, last);
+    if (SCALES) move1<PH>(FA, FB, first, last);
   }
 
   template <int PH>
@@ -187,7 +234,8 @@ struct RRWork {
   double tol2;
   double* part;  // [2][NWARP][2 * NPAIR]
   double* d;     // this warp's NP tracked norms
-  double2* log;  // global cursor (warp 0 writes)
+  double2* log;  // global cursor (warp 0 writes): per step and slot (al, be)
+  double* slog;  // global cursor (warp 0 writes): per sweep the NP column scales
   int ex, sweeps, conv, rot, recompute;
   long long rots;
 
@@ -233,8 +281,14 @@ struct RRWork {
     cross_warp(v);
     if (rot_lane()) {
       const int k = slot();
-      d[rr_col<NP>(k, t)] = v[0];
-      d[rr_col<NP>(NP - 1 - k, t)] = v[1];
+      double fa = tile.FA[RRTile<C>::template ia<PH>(0)], fb = tile.FB[RRTile<C>::template ib<PH>(0)];
+#pragma unroll
+      for (int j = 1; j < S; ++j) {
+        fa = rgl == j ? tile.FA[RRTile<C>::template ia<PH>(j)] : fa;
+        fb = rgl == j ? tile.FB[RRTile<C>::template ib<PH>(j)] : fb;
+      }
+      d[rr_col<NP>(k, t)] = v[0] * (fa * fa);
+      d[rr_col<NP>(NP - 1 - k, t)] = v[1] * (fb * fb);
     }
     __syncwarp();
     recompute = 0;
@@ -254,36 +308,65 @@ struct RRWork {
     warp_sum(g);
     double v[1] = {pick<S>(g, rgl)};
     cross_warp(v);
-    double cc = 1.0, sn = 0.0;
+    double al = 0.0, be = 0.0, cc = 1.0;
     int flag = 0;
     if (rot_lane()) {
       const int k = slot();
+      double fa = tile.FA[RRTile<C>::template ia<PH>(0)], fb = tile.FB[RRTile<C>::template ib<PH>(0)];
+#pragma unroll
+      for (int j = 1; j < S; ++j) {
+        fa = rgl == j ? tile.FA[RRTile<C>::template ia<PH>(j)] : fa;
+        fb = rgl == j ? tile.FB[RRTile<C>::template ib<PH>(j)] : fb;
+      }
       const int ca = rr_col<NP>(k, t), cb = rr_col<NP>(NP - 1 - k, t);
       const bool rev = ca > cb;  // slot a holds the larger column: rotate with swapped roles
       const int p = rev ? cb : ca, q = rev ? ca : cb;
-      const double dpp = d[p], dqq = d[q], gpq = v[0];
+      const double dpp = d[p], dqq = d[q], gpq = v[0] * (fa * fb);
       if (gpq * gpq > tol2 * (dpp * dqq)) {  // skip rule (jacobi.py:167)
-        double tt;
+        double sn, tt;
         jacobi_rotation_t(dpp, gpq, dqq, cc, sn, tt);
         const double np_ = dpp - tt * gpq, nq = dqq + tt * gpq;
         d[p] = np_ > 0.0 ? np_ : 0.0;
         d[q] = nq > 0.0 ? nq : 0.0;
         flag = (np_ < 1e-2 * dpp) | (nq < 1e-2 * dqq);  // cancellation -> recompute next step
-        if (rev) sn = -sn;
+        const double tp = rev ? -tt : tt;               // tangent in position order (a, b)
+        const double rinv = rcp_fast(fa * fb);
+        al = -tp * (fb * fb) * rinv;
+        be = tp * (fa * fa) * rinv;
         ++rot;
       }
-      if (log != nullptr && warp == 0) log[k] = make_double2(cc, sn);
+      if (log != nullptr && warp == 0) log[k] = make_double2(al, be);
     }
     if (log != nullptr) log += NPAIR;
     recompute = __any_sync(FULL, flag);
-    double c[S], s[S];
+    double a[S], b[S], c[S];
 #pragma unroll
     for (int j = 0; j < S; ++j) {
+      a[j] = __shfl_sync(FULL, al, j * SG + sg);
+      b[j] = __shfl_sync(FULL, be, j * SG + sg);
       c[j] = __shfl_sync(FULL, cc, j * SG + sg);
-      s[j] = __shfl_sync(FULL, sn, j * SG + sg);
     }
-    tile.template apply<PH>(c, s);
-    tile.template move<PH>(sg);
+    tile.template apply<PH>(a, b);
+    tile.template scale_update<PH>(c);
+    tile.template move<PH, true>(sg);
+  }
+
+  // end of a sweep (t == 0 again: positions are columns): fold the scales into W, log them
+  // for the V replay, and decide convergence
+  template <int PH>
+  BF_DEV bool sweep_end(RRTile<C>& tile) {
+    if (slog != nullptr) {
+      if (warp == 0 && rgl == 0) {
+#pragma unroll
+        for (int j = 0; j < S; ++j) {
+          slog[sg * S + j] = tile.FA[RRTile<C>::template ia<PH>(j)];
+          slog[NP - 1 - (sg * S + j)] = tile.FB[RRTile<C>::template ib<PH>(j)];
+        }
+      }
+      slog += NP;
+    }
+    tile.renormalize();
+    return sweep_end();
   }
 
   BF_DEV bool sweep_end() {
@@ -316,8 +399,15 @@ struct RRReplay {
     cur = 0;
     in_stage = 0;
   }
+  const double* slog;  // per sweep the NP column scales logged by the W phase
   template <int PH>
   BF_DEV void sweep_start(RRTile<C>&, int) {}
+  template <int PH>
+  BF_DEV bool sweep_end(RRTile<C>& tile) {
+    tile.template scale_cols<PH>(slog, sg);
+    slog += C::NP;
+    return sweep_end();
+  }
   template <int PH>
   BF_DEV void step(RRTile<C>& tile, int) {
     if (in_stage == kRRStage) {
@@ -337,7 +427,7 @@ struct RRReplay {
     }
     ++in_stage;
     tile.template apply<PH>(c, s);
-    tile.template move<PH>(sg);
+    tile.template move<PH, false>(sg);
   }
   BF_DEV bool sweep_end() { return --sweeps_left <= 0; }
 };
@@ -351,7 +441,7 @@ struct RRDriver {
     act.template step<PH>(tile, t);
     if (++t == NP - 1) {
       t = 0;
-      if (act.sweep_end()) return true;
+      if (act.template sweep_end<(PH + 1) % S>(tile)) return true;
       act.template sweep_start<(PH + 1) % S>(tile, 0);
     }
     return false;
@@ -392,6 +482,8 @@ struct RRArgs {
   int max_sweeps;
   double2* log;
   int64_t log_stride;
+  double* slog;  // per CTA slot: max_sweeps x NP column scales
+  int64_t slog_stride;
   const uint8_t* active;
 };
 
@@ -410,8 +502,11 @@ static size_t rr_smem_bytes(int m, int nw) {
   return (d * 8 + 15) & ~(size_t)15;
 }
 
+#ifndef BF_RR_MINB
+#define BF_RR_MINB 1
+#endif
 template <class C>
-__global__ void __launch_bounds__(C::THREADS) svd_rr_kernel(RRArgs<double> a) {
+__global__ void __launch_bounds__(C::THREADS, BF_RR_MINB) svd_rr_kernel(RRArgs<double> a) {
   extern __shared__ __align__(16) double sm[];
   int* ctr = reinterpret_cast<int*>(sm);  // 16 ints: extraction counters
   double* Wsm = sm + 8;
@@ -428,6 +523,7 @@ __global__ void __launch_bounds__(C::THREADS) svd_rr_kernel(RRArgs<double> a) {
     if (a.active && !a.active[b]) continue;  // uniform across the CTA
     const double* Ab = a.a + b * a.a_stride;
     RRTile<C> tile;
+    tile.unit_scales();
 #pragma unroll
     for (int j = 0; j < C::S; ++j) {
       const int ca = sg * C::S + j, cb = C::NP - 1 - (sg * C::S + j);
@@ -454,6 +550,7 @@ __global__ void __launch_bounds__(C::THREADS) svd_rr_kernel(RRArgs<double> a) {
     wk.part = Wsm;
     wk.d = Wsm + RRShared<C>::PART + warp * C::NP;
     wk.log = a.log ? a.log + (int64_t)blockIdx.x * a.log_stride : nullptr;
+    wk.slog = a.log ? a.slog + (int64_t)blockIdx.x * a.slog_stride : nullptr;
     wk.ex = 0;
     wk.sweeps = 0;
     wk.conv = n < 2;
@@ -496,6 +593,7 @@ __global__ void __launch_bounds__(C::THREADS) svd_rr_kernel(RRArgs<double> a) {
       if (wk.sweeps > 0) {
         RRReplay<C> rp;
         rp.log = a.log + (int64_t)blockIdx.x * a.log_stride;
+        rp.slog = a.slog + (int64_t)blockIdx.x * a.slog_stride;
         rp.stage = reinterpret_cast<double2*>(Wsm);
         rp.sg = sg;
         rp.sweeps_left = wk.sweeps;
@@ -533,7 +631,9 @@ static int launch_rr(const SvdLaunch& L, int nw, void* ws, size_t ws_bytes, cuda
   const int grid = (int)(L.batch < cap ? L.batch : cap);
   // the replay prefetches up to two stages past the last logged step
   const int64_t log_stride = ((int64_t)L.max_sweeps * (C::NP - 1) + 2 * kRRStage + 1) * C::NPAIR;
-  const size_t log_bytes = L.v ? (size_t)grid * log_stride * sizeof(double2) : 0;
+  const int64_t slog_stride = (int64_t)L.max_sweeps * C::NP;
+  const size_t log_bytes =
+      L.v ? (size_t)grid * log_stride * sizeof(double2) + (size_t)grid * slog_stride * sizeof(double) : 0;
   if (need) {
     *need = log_bytes;
     return 0;
@@ -560,6 +660,8 @@ static int launch_rr(const SvdLaunch& L, int nw, void* ws, size_t ws_bytes, cuda
   a.max_sweeps = L.max_sweeps;
   a.log = L.v ? (double2*)ws : nullptr;
   a.log_stride = log_stride;
+  a.slog = L.v ? (double*)((double2*)ws + (size_t)grid * log_stride) : nullptr;
+  a.slog_stride = slog_stride;
   a.active = L.active;
   svd_rr_kernel<C><<<grid, C::THREADS, smem, st>>>(a);
   return (int)cudaGetLastError();

@@ -1,1 +1,2 @@
-for st in 16 32; do echo "== stage $st"; BATCHFACT_B200_LIB=build_var/lib_st$st.so python tools/time_variants.py 2>&1 | grep "tier=auto" | grep -v serial; done
+timeout 600 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "svd or block or rsvd" 2>&1 | tail -5
+python tools/time_variants.py 2>&1 | grep "tier=auto" | grep -v serial
