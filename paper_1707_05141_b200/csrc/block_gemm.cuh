@@ -182,4 +182,237 @@ __global__ void __launch_bounds__(256) bj_rot(BJGemmArgs<T> a, int step) {
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// FP64 tensor-core (DMMA, mma.sync.m8n8k4.f64) versions for 2k = 64, the BASELINE block width.
+// Tensor-core fragments (PTX m8n8k4 .f64): lane = 4 g + t holds A[g][t], B[t][g] and
+// D[g][2t], D[g][2t+1]. A CTA of 8 warps owns one (matrix, block pair); warp w computes a 16 x 32
+// block (2 x 4 tiles) of the 64-wide output so each k-step issues 6 fragment loads per 8 DMMAs.
+// Operands are staged column-major in shared memory (row stride padded so the 4 k-rows x 8
+// columns of a fragment load hit two wavefronts) by 16-byte cp.async, double buffered.
+BF_DEV void dmma_8x8x4(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+BF_DEV void cpa16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+BF_DEV void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+BF_DEV void cpa_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+constexpr int kMmaKK = 64;   // pair width 2k
+constexpr int kGramCH = 32;  // rows per staged chunk (8 k-steps)
+constexpr int kGramLD = kGramCH + 4;
+
+// G = P^T P for P = [W_bi W_bj] (m x 64), e = scaled_offdiag(G), activity mask (see bj_gram).
+__global__ void __launch_bounds__(256) bj_gram_mma(BJGemmArgs<double> a, int step) {
+  constexpr int KK = kMmaKK, CH = kGramCH, LDR = kGramLD, LDG = KK + 1;
+  __shared__ __align__(16) double stage[2][KK * LDR];
+  __shared__ double red;
+  double* Gs = &stage[0][0];  // 64 x 65 after the accumulation (fits in the two stages)
+  const int P = a.nb / 2;
+  const int64_t b = blockIdx.x / P;
+  const int pk = blockIdx.x % P;
+  const int64_t slot = blockIdx.x;
+  if (b >= a.batch) return;
+  if (!a.active[b]) {
+    if (threadIdx.x == 0) a.pair_act[slot] = 0;
+    return;
+  }
+  int bi, bj;
+  rr_pair(a.nb, step, pk, bi, bj);
+  const int k = a.k, m = a.m, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int i0 = (warp >> 1) * 16, j0 = (warp & 1) * 32;  // output rows (cols of P) / cols
+  const double* Wb = a.W + b * (int64_t)m * a.n_pad;
+  auto load = [&](int buf, int r0) {
+    // 64 columns x CH rows, 16 B (2 rows) per cp.async; rows past m are zero-filled
+    for (int e = tid; e < KK * CH / 2; e += 256) {
+      const int c = e / (CH / 2), r = 2 * (e % (CH / 2));
+      double* dst = &stage[buf][c * LDR + r];
+      if (r0 + r + 1 < m) {
+        cpa16(dst, Wb + (size_t)bj_pair_col(c, k, bi, bj) * m + r0 + r);
+      } else {
+        dst[0] = r0 + r < m ? Wb[(size_t)bj_pair_col(c, k, bi, bj) * m + r0 + r] : 0.0;
+        dst[1] = 0.0;
+      }
+    }
+    cpa_commit();
+  };
+  double acc[2][4][2];
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  const int nch = (m + CH - 1) / CH;
+  load(0, 0);
+  for (int ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) {
+      load((ch + 1) & 1, (ch + 1) * CH);
+      cpa_wait<1>();
+    } else {
+      cpa_wait<0>();
+    }
+    __syncthreads();
+    const double* S = stage[ch & 1];
+#pragma unroll
+    for (int k0 = 0; k0 < CH; k0 += 4) {
+      double av[2], bv[4];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) av[x] = S[(i0 + 8 * x + g) * LDR + k0 + t];  // A[g][t] = P[k][i]
+#pragma unroll
+      for (int y = 0; y < 4; ++y) bv[y] = S[(j0 + 8 * y + g) * LDR + k0 + t];  // B[t][g] = P[k][j]
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) dmma_8x8x4(acc[x][y], av[x], bv[y]);
+    }
+    __syncthreads();  // stage (ch & 1) is reloaded next iteration
+  }
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      Gs[(i0 + 8 * x + g) * LDG + j0 + 8 * y + 2 * t] = acc[x][y][0];
+      Gs[(i0 + 8 * x + g) * LDG + j0 + 8 * y + 2 * t + 1] = acc[x][y][1];
+    }
+  if (tid == 0) red = 0.0;
+  __syncthreads();
+  // exactly symmetric (core.py:75-77: upper triangle mirrored), column-major out; e on the fly
+  double* Gout = a.G + slot * KK * KK;
+  double best = 0.0;
+  for (int e = tid; e < KK * KK; e += 256) {
+    const int j = e / KK, i = e % KK;  // G[i][j]
+    const double gv = i <= j ? Gs[i * LDG + j] : Gs[j * LDG + i];
+    Gout[e] = gv;
+    if (i != j) {
+      const double den = sqrt(fabs(Gs[i * LDG + i])) * sqrt(fabs(Gs[j * LDG + j]));
+      const double num = fabs(gv);
+      const double rt = den > 0.0 ? num / den : (num > 0.0 ? __longlong_as_double(0x7ff0000000000000LL) : 0.0);
+      best = rt > best ? rt : best;
+    }
+  }
+  best = warp_allreduce_max(best);
+  if ((tid & 31) == 0 && best > 0.0) bj_atomic_max_pos(&red, best);
+  __syncthreads();
+  if (tid == 0) {
+    const double e = red;
+    bj_atomic_max_pos(a.e_sweep + b, e);
+    a.pair_act[slot] = e > a.tol ? 1 : 0;  // pairs at e <= tol are skipped (blockjacobi.py:128-129)
+  }
+}
+
+constexpr int kRotCH = 64;           // rows per chunk
+constexpr int kRotLDX = kRotCH + 8;  // X chunk row stride (column-major, 64 rows)
+constexpr int kRotLDU = kMmaKK + 4;  // U stride (column-major)
+constexpr size_t kRotSmem = (size_t)(kMmaKK * kRotLDU + 2 * kMmaKK * kRotLDX + kMmaKK) * sizeof(double);
+
+// pair <- pair @ U_G (null directions zeroed), V pair <- V pair @ U_G (see bj_rot).
+__global__ void __launch_bounds__(256) bj_rot_mma(BJGemmArgs<double> a, int step) {
+  constexpr int KK = kMmaKK, CH = kRotCH, LDX = kRotLDX, LDU = kRotLDU;
+  extern __shared__ __align__(16) double sm_rot[];
+  double* Us = sm_rot;                // U column-major: U[k][n] at Us[n * LDU + k]
+  double* Xs = Us + KK * LDU;         // 2 chunks, column-major: X[r][c] at Xs[c * LDX + r]
+  double* sig = Xs + 2 * KK * LDX;    // inner sigma (null directions)
+  const int P = a.nb / 2;
+  const int64_t b = blockIdx.x / P;
+  const int pk = blockIdx.x % P;
+  const int64_t slot = blockIdx.x;
+  if (b >= a.batch || !a.pair_act[slot]) return;
+  int bi, bj;
+  rr_pair(a.nb, step, pk, bi, bj);
+  const int k = a.k, m = a.m, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int r0w = (warp >> 1) * 16, c0w = (warp & 1) * 32;
+  const double* Ug = a.U + slot * KK * KK;
+  for (int e = tid; e < KK * KK / 2; e += 256) {
+    const int c = e / (KK / 2), r = 2 * (e % (KK / 2));
+    cpa16(&Us[c * LDU + r], Ug + (size_t)c * KK + r);
+  }
+  cpa_commit();
+  if (tid < KK) sig[tid] = a.S[slot * KK + tid];
+  // the chunk sequence runs over W (m rows) then V (n_pad rows)
+  double* Wm = a.W + b * (int64_t)m * a.n_pad;
+  double* Vm = a.V ? a.V + b * (int64_t)a.n_pad * a.n_pad : nullptr;
+  const int nw_ch = (m + CH - 1) / CH, nv_ch = Vm ? (a.n_pad + CH - 1) / CH : 0, nch = nw_ch + nv_ch;
+  auto where = [&](int ch, double*& M, int& ld, int& rows, int& r0, bool& isw) {
+    isw = ch < nw_ch;
+    M = isw ? Wm : Vm;
+    ld = isw ? m : a.n_pad;
+    rows = ld;
+    r0 = (isw ? ch : ch - nw_ch) * CH;
+  };
+  auto load = [&](int buf, int ch) {
+    double* M;
+    int ld, rows, r0;
+    bool isw;
+    where(ch, M, ld, rows, r0, isw);
+    double* X = Xs + buf * KK * LDX;
+    for (int e = tid; e < KK * CH / 2; e += 256) {
+      const int c = e / (CH / 2), r = 2 * (e % (CH / 2));
+      double* dst = &X[c * LDX + r];
+      const double* src = M + (size_t)bj_pair_col(c, k, bi, bj) * ld + r0 + r;
+      if (r0 + r + 1 < rows) {
+        cpa16(dst, src);
+      } else {
+        dst[0] = r0 + r < rows ? src[0] : 0.0;
+        dst[1] = 0.0;
+      }
+    }
+    cpa_commit();
+  };
+  load(0, 0);
+  for (int ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) {
+      load((ch + 1) & 1, ch + 1);
+      cpa_wait<1>();
+    } else {
+      cpa_wait<0>();
+    }
+    __syncthreads();
+    const double* X = Xs + (ch & 1) * KK * LDX;
+    double acc[2][4][2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+#pragma unroll 4
+    for (int k0 = 0; k0 < KK; k0 += 4) {
+      double av[2], bv[4];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) av[x] = X[(k0 + t) * LDX + r0w + 8 * x + g];  // A[g][t] = X[r][k]
+#pragma unroll
+      for (int y = 0; y < 4; ++y) bv[y] = Us[(c0w + 8 * y + g) * LDU + k0 + t];  // B[t][g] = U[k][n]
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) dmma_8x8x4(acc[x][y], av[x], bv[y]);
+    }
+    double* M;
+    int ld, rows, r0;
+    bool isw;
+    where(ch, M, ld, rows, r0, isw);
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      const int r = r0 + r0w + 8 * x + g;
+      if (r < rows) {
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int c = c0w + 8 * y + 2 * t + q;
+            // keep exactly-null directions exactly null (blockjacobi.py:133-134)
+            const double val = (isw && !(sig[c] != 0.0)) ? 0.0 : acc[x][y][q];
+            M[(size_t)bj_pair_col(c, k, bi, bj) * ld + r] = val;
+          }
+      }
+    }
+    __syncthreads();  // chunk buffer (ch & 1) is reloaded next iteration
+  }
+}
+
 }  // namespace bf

@@ -359,6 +359,12 @@ size_t block_ws_bytes(int dtype, int64_t batch, int m, int n, int block_width, i
                     : bj_layout<float>(batch, m, n, block_width, method, accv).total;
 }
 
+// fp64 with 2k = 64: Gram and rotation products on the FP64 tensor cores (bj_*_mma)
+template <typename T>
+static constexpr bool kUseMma(int TT) {
+  return sizeof(T) == 8 && TT == 4;
+}
+
 template <typename T>
 static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
   BJArgs<T> a;
@@ -444,6 +450,8 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
     if (TT == 2) e = cudaFuncSetAttribute(bj_rot<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rot_smem);
     if (TT == 3) e = cudaFuncSetAttribute(bj_rot<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rot_smem);
     if (TT == 4) e = cudaFuncSetAttribute(bj_rot<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rot_smem);
+    if (e == cudaSuccess && kUseMma<T>(TT))
+      e = cudaFuncSetAttribute(bj_rot_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRotSmem);
     if (e != cudaSuccess) return (int)e;
   }
   void* iws = base + lay.iws;
@@ -455,13 +463,19 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
         if (TT == 1) bj_gram<T, 1><<<grid, 256, 0, st>>>(g, s);
         if (TT == 2) bj_gram<T, 2><<<grid, 256, 0, st>>>(g, s);
         if (TT == 3) bj_gram<T, 3><<<grid, 256, 0, st>>>(g, s);
-        if (TT == 4) bj_gram<T, 4><<<grid, 256, 0, st>>>(g, s);
+        if (kUseMma<T>(TT))
+          bj_gram_mma<<<grid, 256, 0, st>>>(*reinterpret_cast<BJGemmArgs<double>*>(&g), s);
+        else if (TT == 4)
+          bj_gram<T, 4><<<grid, 256, 0, st>>>(g, s);
         int rc = launch_svd(sizeof(T) == 8 ? 0 : 1, in, iws, iws_bytes, st);
         if (rc) return rc;
         if (TT == 1) bj_rot<T, 1><<<grid, 256, rot_smem, st>>>(g, s);
         if (TT == 2) bj_rot<T, 2><<<grid, 256, rot_smem, st>>>(g, s);
         if (TT == 3) bj_rot<T, 3><<<grid, 256, rot_smem, st>>>(g, s);
-        if (TT == 4) bj_rot<T, 4><<<grid, 256, rot_smem, st>>>(g, s);
+        if (kUseMma<T>(TT))
+          bj_rot_mma<<<grid, 256, kRotSmem, st>>>(*reinterpret_cast<BJGemmArgs<double>*>(&g), s);
+        else if (TT == 4)
+          bj_rot<T, 4><<<grid, 256, rot_smem, st>>>(g, s);
       } else if (L.method == 0) {
         bj_gram_step<T><<<grid, 256, smem, st>>>(a, s);
       } else {
