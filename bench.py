@@ -196,7 +196,8 @@ class GpuConfig:
             return 1
         if c["kind"] == "block":
             nb = c["n"] // 32
-            return 1 + 30 * (nb - 1 + 1) + 1  # init + (steps + finalize) x max_sweeps + extract
+            # init + max_sweeps x (steps x (gram, inner svd, rotation) + finalize) + extract
+            return 1 + 30 * (3 * (nb - 1) + 1) + 1
         return 8  # rsvd: gaussian, gemm, qr, gemm, qr, svd, gemm, gemm
 
     def flops(self):

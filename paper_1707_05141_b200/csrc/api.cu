@@ -220,13 +220,14 @@ int rsvd_impl(int64_t batch, int m, int n, int k, int p, uint64_t slo, uint64_t 
   T* Ur = (T*)(base + Ly.ur);
   T* Vr = (T*)(base + Ly.vr);
   void* sws = base + Ly.svdws;
-  if (!omega) {  // gaussian_matrix(n, w, seed ^ i) (rsvd.py:65, :82-85)
-    rc = bf::launch_gaussian_f64(batch, n, w, slo, shi, ibase, 0, 0, (double*)om, (int64_t)n * w, cs);
+  if (!omega) {  // gaussian_matrix(n, w, seed ^ i) (rsvd.py:65, :82-85), kept in C order (row-major)
+    rc = bf::launch_gaussian_f64(batch, n, w, slo, shi, ibase, 0, 0, (double*)om, (int64_t)n * w, cs, 1);
     if (rc) return cuda_rc(rc, "rsvd/omega");
   }
   bf::GemmLaunch g;
-  // Y = A @ Omega (rsvd.py:66)
-  g = bf::GemmLaunch{batch, m, w, n, a, m, (int64_t)m * n, false, om, n, (int64_t)n * w, false, Y, m, (int64_t)m * w};
+  // Y = A @ Omega (rsvd.py:66); a device-drawn Omega is row-major, i.e. Omega^T column-major
+  g = bf::GemmLaunch{batch, m,    w,  n, a, m, (int64_t)m * n, false, om, omega ? n : w, (int64_t)n * w, !omega, Y, m,
+                     (int64_t)m * w};
   if ((rc = bf::launch_gemm(dt, g, cs))) return cuda_rc(rc, "rsvd/gemm1");
   // Q = qr(Y).q (rsvd.py:67)
   if ((rc = bf::launch_qr(dt, batch, m, w, Y, (int64_t)m * w, Q, (int64_t)m * w, R, (int64_t)w * w, sws, cs)))

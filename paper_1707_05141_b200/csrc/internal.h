@@ -63,8 +63,10 @@ int launch_qr(int dtype, int64_t batch, int m, int n, const void* a, int64_t a_s
               void* r, int64_t r_stride, void* ws, cudaStream_t st);
 size_t qr_global_ws_bytes(int dtype, int64_t batch, int m, int n);
 int launch_gemm(int dtype, const GemmLaunch& L, cudaStream_t st);
+// c_order: store the C-order fill contiguously (row-major rows x cols) instead of column-major
 int launch_gaussian_f64(int64_t batch, int rows, int cols, uint64_t seed_lo, uint64_t seed_hi, int64_t index_base,
-                        int seed_mode, uint64_t xor_mask, double* out, int64_t out_stride, cudaStream_t st);
+                        int seed_mode, uint64_t xor_mask, double* out, int64_t out_stride, cudaStream_t st,
+                        int c_order = 0);
 int launch_sign_fix_f64(int64_t batch, int m, int n, double* q, const double* r, cudaStream_t st);
 int launch_scale_cols_f64(int64_t batch, int m, int n, double* q, const double* sigma, cudaStream_t st);
 

@@ -67,8 +67,115 @@ __global__ void __launch_bounds__(256) gemm_kernel(GemmLaunch g) {
   }
 }
 
+// FP64 tensor-core (DMMA m8n8k4) batched GEMM for the tall-skinny products of the randomized SVD
+// (Y = A Omega, B^T = A^T Q, U = Q U_R, V = Q_B V_R: M <= 128, N <= 64): one CTA of 8 warps per
+// matrix, warp w owns row tiles 2w, 2w+1 and all NT column tiles of C; K staged through shared
+// memory in chunks of 16, column-major with padded strides (fragment loads = 2 wavefronts).
+// Fragments: lane = 4 g + t holds A[g][t], B[t][g], D[g][2t + q].
+BF_DEV void dmma884(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+constexpr int kGmKC = 16;            // K chunk
+constexpr int kGmLDA = 128 + 8;      // A chunk: As[k * LDA + i]
+constexpr int kGmLDB = kGmKC + 4;    // B chunk: Bs[j * LDB + k]
+
+template <int NT>
+__global__ void __launch_bounds__(256) gemm_mma_kernel(GemmLaunch g) {
+  __shared__ __align__(16) double As[kGmKC * kGmLDA];
+  __shared__ __align__(16) double Bs[8 * NT * kGmLDB];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, t = lane & 3;
+  const int i0 = warp * 16;
+  for (int64_t b = blockIdx.x; b < g.batch; b += gridDim.x) {
+    const double* A = (const double*)g.a + b * g.a_stride;
+    const double* B = (const double*)g.b + b * g.b_stride;
+    double* C = (double*)g.c + b * g.c_stride;
+    double acc[2][NT][2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < NT; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    for (int k0 = 0; k0 < g.K; k0 += kGmKC) {
+      __syncthreads();
+      if (!g.ta) {  // A column-major M x K: rows contiguous
+        for (int e = tid; e < kGmKC * 128; e += 256) {
+          const int kk = e >> 7, ii = e & 127, gk = k0 + kk;
+          As[kk * kGmLDA + ii] = (ii < g.M && gk < g.K) ? A[(size_t)gk * g.lda + ii] : 0.0;
+        }
+      } else {  // A stored K x M: k contiguous
+        for (int e = tid; e < kGmKC * 128; e += 256) {
+          const int kk = e % kGmKC, ii = e / kGmKC, gk = k0 + kk;
+          As[kk * kGmLDA + ii] = (ii < g.M && gk < g.K) ? A[(size_t)ii * g.lda + gk] : 0.0;
+        }
+      }
+      if (!g.tb) {  // B column-major K x N: k contiguous
+        for (int e = tid; e < kGmKC * 8 * NT; e += 256) {
+          const int kk = e % kGmKC, jj = e / kGmKC, gk = k0 + kk;
+          Bs[jj * kGmLDB + kk] = (jj < g.N && gk < g.K) ? B[(size_t)jj * g.ldb + gk] : 0.0;
+        }
+      } else {  // B stored N x K: j contiguous
+        for (int e = tid; e < kGmKC * 8 * NT; e += 256) {
+          const int jj = e % (8 * NT), kk = e / (8 * NT), gk = k0 + kk;
+          Bs[jj * kGmLDB + kk] = (jj < g.N && gk < g.K) ? B[(size_t)gk * g.ldb + jj] : 0.0;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kq = 0; kq < kGmKC; kq += 4) {
+        double av[2], bv[NT];
+#pragma unroll
+        for (int x = 0; x < 2; ++x) av[x] = As[(kq + t) * kGmLDA + i0 + 8 * x + gq];
+#pragma unroll
+        for (int y = 0; y < NT; ++y) bv[y] = Bs[(8 * y + gq) * kGmLDB + kq + t];
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+          for (int y = 0; y < NT; ++y) dmma884(acc[x][y], av[x], bv[y]);
+      }
+    }
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      const int i = i0 + 8 * x + gq;
+      if (i < g.M) {
+#pragma unroll
+        for (int y = 0; y < NT; ++y)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int j = 8 * y + 2 * t + q;
+            if (j < g.N) C[(size_t)j * g.ldc + i] = acc[x][y][q];
+          }
+      }
+    }
+  }
+}
+
+template <int NT>
+static void launch_gemm_mma(const GemmLaunch& g, cudaStream_t st) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t cap = (int64_t)sms * 8;
+  const unsigned grid = (unsigned)(g.batch < cap ? g.batch : cap);
+  gemm_mma_kernel<NT><<<grid, 256, 0, st>>>(g);
+}
+
 int launch_gemm(int dtype, const GemmLaunch& g, cudaStream_t st) {
   if (g.batch == 0 || g.M == 0 || g.N == 0) return 0;
+  if (dtype == 0 && g.M <= 128 && g.N <= 64) {
+    switch ((g.N + 7) / 8) {
+      case 1: launch_gemm_mma<1>(g, st); break;
+      case 2: launch_gemm_mma<2>(g, st); break;
+      case 3: launch_gemm_mma<3>(g, st); break;
+      case 4: launch_gemm_mma<4>(g, st); break;
+      case 5: launch_gemm_mma<5>(g, st); break;
+      case 6: launch_gemm_mma<6>(g, st); break;
+      case 7: launch_gemm_mma<7>(g, st); break;
+      default: launch_gemm_mma<8>(g, st); break;
+    }
+    return (int)cudaGetLastError();
+  }
   int tiles = ((g.M + 63) / 64) * ((g.N + 63) / 64);
   unsigned gy = (unsigned)(g.batch < 65535 ? g.batch : 65535);
   if (dtype == 0)
@@ -81,12 +188,14 @@ int launch_gemm(int dtype, const GemmLaunch& g, cudaStream_t st) {
 // ------------------------------------------------------------------ Gaussian sampler
 // numpy Generator(Philox(key=seed)).standard_normal((rows, cols)) (rsvd.py:42-53):
 // Philox4x64-10 stream (counter incremented before each 4-word block), float64
-// ziggurat (numpy random_standard_normal), C-order fill, stored column-major.
-// One warp per matrix: lanes test 32 consecutive stream words against the
-// ziggurat fast path in parallel; the rare slow path is walked by lane 0.
+// ziggurat (numpy random_standard_normal), C-order fill.
+// One warp per matrix: each lane computes one Philox block (4 consecutive stream words), so a
+// warp tests 128 words against the ziggurat fast path at once; accepted samples are compacted
+// by a warp prefix sum and stored contiguously (C order) or transposed (column-major). The rare
+// slow path (~1.2% of words: wedge / tail) is walked by lane 0 and the warp resumes after it.
 
-BF_DEV uint64_t philox_word(uint64_t k0, uint64_t k1, uint64_t pos) {
-  uint64_t c0 = (pos >> 2) + 1, c1 = 0, c2 = 0, c3 = 0;
+BF_DEV void philox_block(uint64_t k0, uint64_t k1, uint64_t blk, uint64_t (&w)[4]) {
+  uint64_t c0 = blk + 1, c1 = 0, c2 = 0, c3 = 0;
   if (c0 == 0) c1 = 1;
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
@@ -100,11 +209,20 @@ BF_DEV uint64_t philox_word(uint64_t k0, uint64_t k1, uint64_t pos) {
     k0 += 0x9E3779B97F4A7C15ULL;
     k1 += 0xBB67AE8584CAA73BULL;
   }
+  w[0] = c0;
+  w[1] = c1;
+  w[2] = c2;
+  w[3] = c3;
+}
+
+BF_DEV uint64_t philox_word(uint64_t k0, uint64_t k1, uint64_t pos) {
+  uint64_t w[4];
+  philox_block(k0, k1, pos >> 2, w);
   switch (pos & 3) {
-    case 0: return c0;
-    case 1: return c1;
-    case 2: return c2;
-    default: return c3;
+    case 0: return w[0];
+    case 1: return w[1];
+    case 2: return w[2];
+    default: return w[3];
   }
 }
 
@@ -112,7 +230,7 @@ BF_DEV double u01(uint64_t r) { return (double)(r >> 11) * (1.0 / 90071992547409
 
 __global__ void gaussian_kernel(int64_t batch, int rows, int cols, uint64_t seed_lo, uint64_t seed_hi,
                                 int64_t index_base, int seed_mode, uint64_t xor_mask, double* out,
-                                int64_t out_stride) {
+                                int64_t out_stride, int c_order) {
   const int lane = threadIdx.x & 31;
   const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (b >= batch) return;
@@ -121,36 +239,67 @@ __global__ void gaussian_kernel(int64_t batch, int rows, int cols, uint64_t seed
   const uint64_t k1 = seed_hi;
   double* o = out + b * out_stride;
   const int64_t total = (int64_t)rows * cols;
+  auto store = [&](int64_t kk, double v) {
+    if (kk < total) {
+      if (c_order)
+        o[kk] = v;
+      else
+        o[(kk % cols) * rows + kk / cols] = v;
+    }
+  };
   int64_t k = 0;
   uint64_t pos = 0;
   while (k < total) {
-    uint64_t r = philox_word(k0, k1, pos + lane);
-    int idx = (int)(r & 0xff);
-    uint64_t rr = r >> 8;
-    int sign = (int)(rr & 1);
-    uint64_t rabs = (rr >> 1) & 0x000fffffffffffffULL;
-    double x = (double)rabs * bf_zig_wi[idx];
-    if (sign) x = -x;
-    bool fast = rabs < bf_zig_ki[idx];
-    unsigned bal = __ballot_sync(FULL, !fast);
-    int L = bal ? __ffs(bal) - 1 : 32;
-    if (lane < L && k + lane < total) {
-      int64_t kk = k + lane;
-      o[(kk % cols) * rows + kk / cols] = x;
+    const uint64_t blk = pos >> 2;
+    const int off = lane == 0 ? (int)(pos & 3) : 0;  // words of lane 0 before pos are consumed
+    uint64_t w[4];
+    philox_block(k0, k1, blk + lane, w);
+    double x[4];
+    int rej = 4;  // first (valid) word of this lane failing the fast path
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint64_t r = w[q];
+      const int idx = (int)(r & 0xff);
+      const uint64_t rr = r >> 8;
+      const uint64_t rabs = (rr >> 1) & 0x000fffffffffffffULL;
+      double v = (double)rabs * bf_zig_wi[idx];
+      x[q] = (rr & 1) ? -v : v;
+      if (q >= off && rej == 4 && !(rabs < bf_zig_ki[idx])) rej = q;
     }
+    const unsigned bal = __ballot_sync(FULL, rej < 4);
+    const int L = bal ? __ffs(bal) - 1 : 32;
+    const int cnt = lane < L ? 4 - off : (lane == L ? rej - off : 0);
+    int incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, d);
+      if (lane >= d) incl += y;
+    }
+    const int start = incl - cnt;
+    const int tot = __shfl_sync(FULL, incl, 31);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q >= off && q - off < cnt) store(k + start + (q - off), x[q]);
+    k += tot;
     if (L == 32) {
-      k += 32;
-      pos += 32;
+      pos = (blk + 32) * 4;
       continue;
     }
-    // slow path for the candidate at stream position pos + L (lane L holds it)
-    double xs = __shfl_sync(FULL, x, L);
-    uint64_t rabs_s = __shfl_sync(FULL, rabs, L);
-    int idx_s = __shfl_sync(FULL, idx, L);
-    uint64_t p = pos + L + 1;
+    // slow path for the candidate word (L, rej_L)
+    const int q_s = __shfl_sync(FULL, rej, L);
+    uint64_t r_s = w[0];
+#pragma unroll
+    for (int q = 1; q < 4; ++q) r_s = q == q_s ? w[q] : r_s;
+    r_s = __shfl_sync(FULL, r_s, L);
+    uint64_t p = (blk + L) * 4 + q_s + 1;
     int produced = 0;
-    double val = 0.0;
-    if (lane == 0) {
+    if (lane == 0 && k < total) {
+      const int idx_s = (int)(r_s & 0xff);
+      const uint64_t rr = r_s >> 8;
+      const uint64_t rabs_s = (rr >> 1) & 0x000fffffffffffffULL;
+      double xs = (double)rabs_s * bf_zig_wi[idx_s];
+      if (rr & 1) xs = -xs;
+      double val = 0.0;
       if (idx_s == 0) {
         for (;;) {
           double xx = -BF_ZIG_NOR_INV_R * log1p(-u01(philox_word(k0, k1, p)));
@@ -170,25 +319,23 @@ __global__ void gaussian_kernel(int64_t batch, int rows, int cols, uint64_t seed
           produced = 1;
         }
       }
-      if (produced && k + L < total) {
-        int64_t kk = k + L;
-        o[(kk % cols) * rows + kk / cols] = val;
-      }
+      if (produced) store(k, val);
     }
     produced = __shfl_sync(FULL, produced, 0);
     p = __shfl_sync(FULL, p, 0);
-    k += L + produced;
+    k += produced;
     pos = p;
   }
 }
 
 int launch_gaussian_f64(int64_t batch, int rows, int cols, uint64_t seed_lo, uint64_t seed_hi, int64_t index_base,
-                        int seed_mode, uint64_t xor_mask, double* out, int64_t out_stride, cudaStream_t st) {
+                        int seed_mode, uint64_t xor_mask, double* out, int64_t out_stride, cudaStream_t st,
+                        int c_order) {
   if (batch == 0 || rows == 0 || cols == 0) return 0;
   const int wpb = 4;
   unsigned grid = (unsigned)((batch + wpb - 1) / wpb);
   gaussian_kernel<<<grid, wpb * 32, 0, st>>>(batch, rows, cols, seed_lo, seed_hi, index_base, seed_mode, xor_mask,
-                                               out, out_stride);
+                                               out, out_stride, c_order);
   return (int)cudaGetLastError();
 }
 
