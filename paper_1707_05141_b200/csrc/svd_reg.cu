@@ -145,11 +145,14 @@ __global__ void __launch_bounds__(C::threads, BF_REG_MINB) svd_reg_kernel(RegArg
         const int col = ORD == 0 ? ((x - off0) % NP + NP) % NP : x;
         v[x] = col == row ? T(1) : T(0);
       }
-      if (act.sweeps > 0) {
+      // a converged run ends with a rotation-free sweep (identity rotations; a full sweep
+      // realigns every column): the replay drops it
+      const int vsweeps = act.sweeps - (act.conv ? 1 : 0);
+      if (vsweeps > 0) {
         VAction<T, C, ORD, kStage> va;
         va.log = a.log + (int64_t)blockIdx.x * a.log_stride;
         va.stage = stage;
-        va.sweeps_left = act.sweeps;
+        va.sweeps_left = vsweeps;
         va.start();
         RegDriver<T, C, ORD>::run(v, n, va);
         cp_async_wait_all();  // the last prefetch (past the end of the log) must land before reuse

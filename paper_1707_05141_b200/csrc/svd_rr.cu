@@ -590,13 +590,15 @@ __global__ void __launch_bounds__(C::THREADS, BF_RR_MINB) svd_rr_kernel(RRArgs<d
       }
       int vph = 0;
       __syncthreads();  // extraction done with the work region (stage lives there)
-      if (wk.sweeps > 0) {
+      if (wk.sweeps - (wk.conv ? 1 : 0) > 0) {
         RRReplay<C> rp;
         rp.log = a.log + (int64_t)blockIdx.x * a.log_stride;
         rp.slog = a.slog + (int64_t)blockIdx.x * a.slog_stride;
         rp.stage = reinterpret_cast<double2*>(Wsm);
         rp.sg = sg;
-        rp.sweeps_left = wk.sweeps;
+        // a converged run ends with a rotation-free sweep: identity rotations and unit scales,
+        // and a full sweep returns every column to its position -- the replay can drop it
+        rp.sweeps_left = wk.sweeps - (wk.conv ? 1 : 0);
         rp.start();
         vph = RRDriver<C, RRReplay<C>>::run(tile, rp);
         cp_async_wait_all();
