@@ -1,0 +1,63 @@
+"""Host-buffer batched calls with copy/compute overlap.
+
+The reference's batch functions take host arrays and return host arrays
+(/root/reference/pkg/src/batchfact/core.py:97-123). On the GPU the round trip
+(host -> HBM -> kernels -> HBM -> host) is bounded by the PCIe copies, so a large
+batch is cut into chunks that flow through three CUDA streams: the host-to-device
+copy of chunk c+1 and the device-to-host copy of chunk c-1 run while chunk c is being
+factorised (two compute streams alternate so one chunk's tail overlaps the next one's
+start). Every chunk is ONE C-ABI call; the per-entry results do not depend on the
+chunking (entries are independent, core.py:97-103), so the output is identical to a
+single call.
+"""
+
+import torch
+
+from .core import resolve_device
+
+
+def run_host_pipelined(op, host_in, host_outs, *, chunks=4, device=None, index_base=0):
+    """Run ``op`` over ``host_in`` chunk by chunk with overlapped copies.
+
+    op(dev_chunk, index_base) -> list of device tensors whose leading dim is the chunk size,
+        in the order of ``host_outs``;
+    host_in: (B, ...) pinned host tensor (the call's input, e.g. column-major storage);
+    host_outs: list of (B, ...) pinned host tensors receiving the results.
+    Returns ``host_outs`` after all copies have completed.
+    """
+    dev = resolve_device(device)
+    B = host_in.shape[0]
+    if B == 0:
+        return host_outs
+    chunks = max(1, min(int(chunks), B))
+    size = -(-B // chunks)
+    bounds = [(s, min(B, s + size)) for s in range(0, B, size)]
+    with torch.cuda.device(dev):
+        s_in = torch.cuda.Stream(dev)
+        s_out = torch.cuda.Stream(dev)
+        s_comp = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+        main = torch.cuda.current_stream(dev)
+        for s in (s_in, s_out, *s_comp):
+            s.wait_stream(main)
+        dev_in = torch.empty(host_in.shape, dtype=host_in.dtype, device=dev)
+        keep = []
+        for c, (lo, hi) in enumerate(bounds):
+            ev_in = torch.cuda.Event()
+            with torch.cuda.stream(s_in):
+                dev_in[lo:hi].copy_(host_in[lo:hi], non_blocking=True)
+                ev_in.record(s_in)
+            sc = s_comp[c & 1]
+            sc.wait_event(ev_in)
+            ev_done = torch.cuda.Event()
+            with torch.cuda.stream(sc):
+                outs = op(dev_in[lo:hi], index_base + lo)
+                ev_done.record(sc)
+            s_out.wait_event(ev_done)
+            with torch.cuda.stream(s_out):
+                for h, d in zip(host_outs, outs):
+                    h[lo:hi].copy_(d, non_blocking=True)
+            keep.append(outs)  # device results stay alive until their copies have run
+        s_out.synchronize()
+        main.wait_stream(s_out)
+        del keep
+    return host_outs

@@ -297,3 +297,31 @@ def test_make_matrix_matches_reference():
 def test_rsvd_errors():
     with pytest.raises(ValueError):
         bf.rsvd(np.ones((8, 6)), bf.RsvdOptions(k=5, p=2))
+
+
+def test_host_pipeline_matches_single_call():
+    """Chunked host-buffer pipeline (stream.py) == one device call, bitwise, incl. rsvd seeds."""
+    from paper_1707_05141_b200.jacobi import svd_colmajor
+    from paper_1707_05141_b200.rsvd import rsvd_colmajor
+    from paper_1707_05141_b200.stream import run_host_pipelined
+
+    a = dev_gauss(37, 24, 24, 77_000)
+    st = a.transpose(1, 2).contiguous()
+    opts = bf.JacobiOptions(ordering="round_robin", accumulate_v=True)
+    ref = svd_colmajor(st, 24, 24, opts)
+    host_in = st.cpu().pin_memory()
+    outs = [torch.empty(ref[k].shape, dtype=ref[k].dtype).pin_memory() for k in ("u", "s", "v", "sweeps")]
+
+    def op(x, ib):
+        r = svd_colmajor(x, 24, 24, opts)
+        return [r["u"], r["s"], r["v"], r["sweeps"]]
+
+    run_host_pipelined(op, host_in, outs, chunks=5)
+    for k, h in zip(("u", "s", "v", "sweeps"), outs):
+        assert torch.equal(h, ref[k].cpu()), k
+    ro = bf.RsvdOptions(k=4, p=2, seed=11)
+    rref = rsvd_colmajor(st, 24, 24, ro, index_base=3)
+    outs = [torch.empty(rref["s"].shape, dtype=torch.float64).pin_memory()]
+    run_host_pipelined(lambda x, ib: [rsvd_colmajor(x, 24, 24, ro, index_base=ib)["s"]], host_in, outs, chunks=4,
+                       index_base=3)
+    assert torch.equal(outs[0], rref["s"].cpu())
