@@ -1,9 +1,12 @@
+# Round measurement: GPU tests, bench (full, with CPU baselines), ncu launch lists per config
+# (the bench command for the headline), one ncu --set full of the headline kernel.
 set -x
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
-tail -5 gpurun_out/pytest_gpu.log
+tail -3 gpurun_out/pytest_gpu.log
 timeout 900 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.log 2>&1; echo "bench rc=$?"
-tail -3 gpurun_out/bench.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_bench_cfg3.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-extra > /dev/null 2>&1; echo "ncu bench rc=$?"
 for c in cfg1 cfg2 cfg3 cfg4 cfg5; do
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$c.csv python tools/prof_run.py $c 2 > /dev/null 2>&1; echo "ncu $c rc=$?"
 done
+bash tools/gpu_ncu_one.sh cfg3_svd_rr cfg3 svd_rr_kernel

@@ -38,8 +38,9 @@ KEYS = {
 STALL_PREFIX = "smsp__average_warp_latency_issue_stalled_"
 STALL_PREFIX2 = "smsp__pcsamp_warps_issue_stalled_"
 
+# capture -> bench config whose dominant kernel it is (later entries win)
 CONFIG_OF = {"cfg1_svd_reg": "cfg1", "cfg2_qr_reg": "cfg2", "cfg3_svd_reg": "cfg3", "cfg4_svd_reg": "cfg4",
-             "cfg5_qr_reg": "cfg5"}
+             "cfg5_qr_reg": "cfg5", "cfg3_svd_rr": "cfg3"}
 
 
 def num(x):
@@ -96,7 +97,7 @@ def main(src, js, md):
             except StopIteration:
                 pass
     by_cfg = {}
-    for name, r in res.items():
+    for name, r in sorted(res.items(), key=lambda kv: list(CONFIG_OF).index(kv[0]) if kv[0] in CONFIG_OF else -1):
         cfg = CONFIG_OF.get(name)
         if cfg:
             by_cfg[cfg] = {"kernel": r["kernel"],
