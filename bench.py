@@ -252,8 +252,8 @@ class GpuConfig:
         chunked so the copies overlap the kernels (paper_1707_05141_b200.stream)."""
         from paper_1707_05141_b200.stream import run_host_pipelined
 
-        run_host_pipelined(self.device_op(), host_in, pinned_out, chunks=chunks, device=self.dev,
-                           index_base=self.plan.start)
+        run_host_pipelined(self.device_op(), host_in, pinned_out, chunks=abs(chunks), device=self.dev,
+                           index_base=self.plan.start, taper=chunks > 0)
         return sum(o.numel() * o.element_size() for o in pinned_out)
 
 
@@ -354,7 +354,7 @@ def main():
     ap.add_argument("--config", default=HEADLINE, help="headline config (cfg1..cfg5)")
     ap.add_argument("--no-extra", action="store_true", help="skip the other configs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--e2e-chunks", type=int, default=4, help="host-buffer pipeline chunks for the e2e leg")
+    ap.add_argument("--e2e-chunks", type=int, default=-8, help="host-buffer pipeline chunks for the e2e leg (negative: equal chunks, no taper)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -432,7 +432,7 @@ def main():
     achieved_tf = flops / t_launch / 1e12
     prof = load_profile(name)
     # e2e through the public API with host buffers
-    e2e_steps = max(1, min(args.steps, 3))
+    e2e_steps = max(5, args.steps)  # host-side timing: more steps than the device leg
     t_e2e, h2d, d2h = time_e2e(gc, e2e_steps, args.e2e_chunks)
     e2e_v = max_over_ranks(t_e2e)
     e2e_value = world * B * e2e_steps / e2e_v

@@ -16,7 +16,38 @@ import torch
 from .core import resolve_device
 
 
-def run_host_pipelined(op, host_in, host_outs, *, chunks=4, device=None, index_base=0):
+def chunk_bounds(B, chunks, taper=True):
+    """Chunk boundaries: ``chunks`` pieces, the first and last half-sized when ``taper`` (the
+    pipeline fill and drain are one chunk's copy each, so short end chunks shorten both)."""
+    chunks = max(1, min(int(chunks), B))
+    if not taper or chunks < 3:
+        size = -(-B // chunks)
+        return [(s, min(B, s + size)) for s in range(0, B, size)]
+    w = [0.5] + [1.0] * (chunks - 2) + [0.5]
+    tot = sum(w)
+    edges = [0]
+    acc = 0.0
+    for x in w[:-1]:
+        acc += x
+        edges.append(int(round(B * acc / tot)))
+    edges.append(B)
+    return [(a, b) for a, b in zip(edges, edges[1:]) if b > a]
+
+
+_STREAMS = {}
+
+
+def _streams(dev):
+    """One set of pipeline streams per device, reused across calls so the caching allocator can
+    recycle the per-stream blocks of earlier calls (fresh streams would force new cudaMallocs)."""
+    key = dev.index
+    if key not in _STREAMS:
+        _STREAMS[key] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev),
+                         torch.cuda.Stream(dev))
+    return _STREAMS[key]
+
+
+def run_host_pipelined(op, host_in, host_outs, *, chunks=4, device=None, index_base=0, taper=False):
     """Run ``op`` over ``host_in`` chunk by chunk with overlapped copies.
 
     op(dev_chunk, index_base) -> list of device tensors whose leading dim is the chunk size,
@@ -29,13 +60,10 @@ def run_host_pipelined(op, host_in, host_outs, *, chunks=4, device=None, index_b
     B = host_in.shape[0]
     if B == 0:
         return host_outs
-    chunks = max(1, min(int(chunks), B))
-    size = -(-B // chunks)
-    bounds = [(s, min(B, s + size)) for s in range(0, B, size)]
+    bounds = chunk_bounds(B, chunks, taper)
     with torch.cuda.device(dev):
-        s_in = torch.cuda.Stream(dev)
-        s_out = torch.cuda.Stream(dev)
-        s_comp = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+        s_in, s_out, c0, c1 = _streams(dev)
+        s_comp = [c0, c1]
         main = torch.cuda.current_stream(dev)
         for s in (s_in, s_out, *s_comp):
             s.wait_stream(main)
