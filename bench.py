@@ -476,7 +476,7 @@ def main():
             g2 = GpuConfig(other, oc, device, rank, world)
             barrier()
             st = 2 if oc["kind"] == "block" else 3
-            t2 = time_gpu(g2, st, 1, flush)
+            t2 = time_gpu(g2, st, 3, flush)
             t2m = max_over_ranks(t2)
             f2, b2 = g2.flops()
             ent = {"desc": oc["desc"], "value": world * oc["batch"] * st / t2m, "unit": UNIT,
