@@ -338,6 +338,9 @@ struct RRWork {
       if (log != nullptr && warp == 0) log[k] = make_double2(al, be);
     }
     if (log != nullptr) log += NPAIR;
+    // order this step's d updates before the next step's reads by other lanes (with several
+    // warps the next step's cross-warp barrier already does; racecheck-clean either way)
+    if (NWARP == 1) __syncwarp();
     recompute = __any_sync(FULL, flag);
     double a[S], b[S], c[S];
 #pragma unroll
