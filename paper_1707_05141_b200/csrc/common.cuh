@@ -53,6 +53,33 @@ BF_DEV double rsqrt_fast(double x) {
   return fma(y, t, y);
 }
 
+// householder_vector's scalars (qr.py:26-48) on the fast reciprocal paths:
+// beta = -copysign(hypot(alpha, sqrt(tail_sq)), alpha), tau = (beta - alpha) / beta, and
+// 1 / (alpha - beta) for v = x / (alpha - beta); IEEE fallback outside [1e-150, 1e150].
+BF_DEV void householder_scalars(double alpha, double tail_sq, double& beta, double& tau, double& denom,
+                                double& rden) {
+  const double q = fma(alpha, alpha, tail_sq);
+  if (q > 1e-300 && q < 1e300) {
+    const double h = q * rsqrt_fast(q);  // hypot(alpha, ||tail||)
+    beta = -copysign(h, alpha);
+    denom = alpha - beta;
+    const double rb = rcp_fast(beta);
+    const double tq = (beta - alpha) * rb;  // (beta - alpha) / beta, one Newton correction:
+    tau = fma(fma(-tq, beta, beta - alpha), rb, tq);
+    rden = rcp_fast(denom);
+  } else {
+    beta = -copysign(hypot(alpha, sqrt(tail_sq)), alpha);
+    tau = (beta - alpha) / beta;
+    denom = alpha - beta;
+    rden = 1.0 / denom;
+  }
+}
+// x / d from a reciprocal r ~ 1/d with one Newton correction of the quotient (<= 1 ulp).
+BF_DEV double div_by(double x, double d, double r) {
+  const double q = x * r;
+  return fma(fma(-q, d, x), r, q);
+}
+
 // Rutishauser rotation (jacobi.py:68-80) for g_pq != 0:
 //   zeta = (g_qq - g_pp) / (2 g_pq); t = sign(zeta) / (|zeta| + hypot(1, zeta));
 //   c = 1 / hypot(1, t); s = c t.

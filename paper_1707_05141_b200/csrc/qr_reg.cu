@@ -108,15 +108,14 @@ struct QrReg {
     wbar(WW);
     double tj = 0.0;
     if (J + 1 < m && tail_sq != 0.0) {  // uniform
-      const double beta = -copysign(hypot(alpha, sqrt(tail_sq)), alpha);
-      tj = (beta - alpha) / beta;
-      const double denom = alpha - beta;
+      double beta, denom, rden;
+      householder_scalars(alpha, tail_sq, beta, tj, denom, rden);
       double acc = 0.0;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int row = tid + r * WW * 32;
         if (row > J && row < m) {
-          const double vi = a[r][J] / denom;
+          const double vi = div_by(a[r][J], denom, rden);
           acc = fma(vi, a[r][J], acc);
           a[r][J] = vi;  // reflector stored below the diagonal
         }
