@@ -198,7 +198,7 @@ class GpuConfig:
             nb = c["n"] // 32
             # init + max_sweeps x (steps x (gram, inner svd, rotation) + finalize) + extract
             return 1 + 30 * (3 * (nb - 1) + 1) + 1
-        return 8  # rsvd: gaussian, gemm, qr, gemm, qr, svd, gemm, gemm
+        return 9  # rsvd: gaussian, gemm, qr, gemm, qr, svd (+ V replay), gemm, gemm
 
     def flops(self):
         """Algorithmic flops of the last step (counted from the run's own sweep/rotation counters)."""
@@ -425,9 +425,9 @@ def main():
     value = world * B * args.steps / t_max
     flops, bytes_alg = gc.flops()
     ms = 1e3 * t_max / args.steps
-    # the headline step is ONE launch of the dominant kernel on the current stream (the C-ABI
-    # call launches exactly one kernel for svd/qr), so the per-step CUDA-event time is the
-    # kernel's launch duration
+    # the headline step is one C-ABI call = the sweep kernel + the V-replay kernel back to back on
+    # the current stream; the CUDA-event time of the step is their combined duration (the sweep
+    # kernel is ~2/3 of it, profiles/launches_r01.md)
     t_launch = t_dev / args.steps
     achieved_tf = flops / t_launch / 1e12
     prof = load_profile(name)
@@ -444,7 +444,8 @@ def main():
             "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
                          "frac": achieved_tf / peaks["fp64_tflops"],
                          "traffic": prof.get("dram_bytes_per_launch"),
-                         "kernel": prof.get("kernel", gc.kernel_name()),
+                         "kernel": gc.kernel_name(),
+                         "traffic_kernel": prof.get("kernel"),
                          "launches_per_step": gc.launches_per_step(),
                          "flops_per_launch": flops, "alg_bytes_per_launch": bytes_alg,
                          "peak_source": "FP64 compute roof: FP64 tensor-core (DMMA) loop measured on this pool, "

@@ -9,4 +9,8 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 for c in cfg1 cfg2 cfg3 cfg4 cfg5; do
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$c.csv python tools/prof_run.py $c 2 > /dev/null 2>&1; echo "ncu $c rc=$?"
 done
-bash tools/gpu_ncu_one.sh cfg3_svd_rr cfg3 svd_rr_kernel
+bash tools/gpu_ncu_one.sh cfg3_svd_rr cfg3 "svd_rr_kernel"
+bash tools/gpu_ncu_one.sh cfg3_svd_rr_v cfg3 "svd_rr_vkernel"
+bash tools/gpu_ncu_one.sh cfg2_qr_reg2 cfg2 "qr_reg_kernel"
+bash tools/gpu_ncu_one.sh cfg4_bj_rot_mma cfg4 "bj_rot_mma" 3
+bash tools/gpu_ncu_one.sh cfg5_gemm_mma cfg5 "gemm_mma" 1

@@ -20,8 +20,8 @@ KEYS = {
     "sm_throughput_pct": ["sm__throughput.avg.pct_of_peak_sustained_elapsed"],
     "fp64_pipe_pct": ["sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
                       "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"],
-    "dmma_pipe_pct": ["sm__pipe_tensor_op_dmma_cycles_active.avg.pct_of_peak_sustained_active",
-                      "sm__pipe_fp64_tensor_cycles_active.avg.pct_of_peak_sustained_active"],
+    "dmma_pipe_pct": ["sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active",
+                      "sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active"],
     "dfma_inst": ["smsp__sass_thread_inst_executed_op_dfma_pred_on.sum"],
     "dadd_inst": ["smsp__sass_thread_inst_executed_op_dadd_pred_on.sum"],
     "dmul_inst": ["smsp__sass_thread_inst_executed_op_dmul_pred_on.sum"],
@@ -41,6 +41,9 @@ STALL_PREFIX2 = "smsp__pcsamp_warps_issue_stalled_"
 # capture -> bench config whose dominant kernel it is (later entries win)
 CONFIG_OF = {"cfg1_svd_reg": "cfg1", "cfg2_qr_reg": "cfg2", "cfg3_svd_reg": "cfg3", "cfg4_svd_reg": "cfg4",
              "cfg5_qr_reg": "cfg5", "cfg3_svd_rr": "cfg3"}
+
+
+CONFIG_SUM = {"cfg3": ["cfg3_svd_rr", "cfg3_svd_rr_v"]}
 
 
 def num(x):
@@ -104,15 +107,24 @@ def main(src, js, md):
                            "dram_bytes_per_launch": (r.get("dram_read", 0) + r.get("dram_write", 0)) or None,
                            "duration_ns_ncu": r.get("duration_ns"),
                            "source": f"ncu --set full capture {name} (profiles/ncu_full_r01.md)"}
+    # configs whose step launches several kernels: traffic = sum over the captured launches
+    for cfg, parts in CONFIG_SUM.items():
+        if all(p in res for p in parts):
+            by_cfg[cfg] = {"kernel": " + ".join(res[p]["kernel"].split("(")[0] for p in parts),
+                           "dram_bytes_per_launch": sum(res[p].get("dram_read", 0) + res[p].get("dram_write", 0)
+                                                        for p in parts),
+                           "duration_ns_ncu": sum(res[p].get("duration_ns", 0) for p in parts),
+                           "source": "ncu --set full captures " + ", ".join(parts) + " (profiles/ncu_full_r01.md)"}
     json.dump({"captures": res, **by_cfg}, open(js, "w"), indent=1)
-    lines = ["| capture | kernel | ncu dur (us) | DRAM R+W (MB) | DRAM % | FP64 pipe % | occupancy % | regs | local ld/st sectors | top stalls |",
-             "|---|---|---:|---:|---:|---:|---:|---:|---|---|"]
+    lines = ["| capture | kernel | ncu dur (us) | DRAM R+W (MB) | DRAM % | FP64 pipe % | DMMA pipe % | occupancy % | regs | local ld/st sectors | top stalls |",
+             "|---|---|---:|---:|---:|---:|---:|---:|---:|---|---|"]
     for name, r in res.items():
         k = r["kernel"].split("(")[0][:60]
         dram = (r.get("dram_read", 0) + r.get("dram_write", 0)) / 1e6
         st = ", ".join(f"{a} {b:.0%}" for a, b in list(r["stall_top"].items())[:4])
         lines.append(f"| {name} | `{k}` | {r.get('duration_ns', 0) / 1e3:.1f} | {dram:.2f} | {r.get('dram_pct_peak', 0):.1f} | "
-                     f"{r.get('fp64_pipe_pct', float('nan')):.1f} | {r.get('achieved_occupancy_pct', 0):.1f} | "
+                     f"{r.get('fp64_pipe_pct', float('nan')):.1f} | {r.get('dmma_pipe_pct', 0):.1f} | "
+                     f"{r.get('achieved_occupancy_pct', 0):.1f} | "
                      f"{r.get('registers', 0):.0f} | {r.get('local_load_sectors', 0):.0f}/{r.get('local_store_sectors', 0):.0f} | {st} |")
     open(md, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
