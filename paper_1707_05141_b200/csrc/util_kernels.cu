@@ -69,71 +69,107 @@ __global__ void __launch_bounds__(256) gemm_kernel(GemmLaunch g) {
 
 // FP64 tensor-core (DMMA m8n8k4) batched GEMM for the tall-skinny products of the randomized SVD
 // (Y = A Omega, B^T = A^T Q, U = Q U_R, V = Q_B V_R: M <= 128, N <= 64): one CTA of 8 warps per
-// matrix, warp w owns row tiles 2w, 2w+1 and all NT column tiles of C; K staged through shared
-// memory in chunks of 16, column-major with padded strides (fragment loads = 2 wavefronts).
+// matrix, warp w owns row tiles 2w, 2w+1 and all NT column tiles of C. K is staged in chunks of
+// 16 by 16-byte cp.async (zero-filled past M / N / K), double buffered; each operand keeps its
+// global contiguity in shared memory (A: k-major when not transposed, i-major when transposed;
+// B likewise), with padded strides so a fragment load is two wavefronts.
 // Fragments: lane = 4 g + t holds A[g][t], B[t][g], D[g][2t + q].
 BF_DEV void dmma884(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
 }
+BF_DEV void cpa16z(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 16 : 0;  // src-size 0: zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(n) : "memory");
+}
 
-constexpr int kGmKC = 16;            // K chunk
-constexpr int kGmLDA = 128 + 8;      // A chunk: As[k * LDA + i]
-constexpr int kGmLDB = kGmKC + 4;    // B chunk: Bs[j * LDB + k]
+constexpr int kGmKC = 16;          // K chunk
+constexpr int kGmLDAk = 128 + 8;   // A, not transposed: As[k * LDAk + i]
+constexpr int kGmLDAi = kGmKC + 4; // A, transposed:     As[i * LDAi + k]
+constexpr int kGmLDBk = kGmKC + 4; // B, not transposed: Bs[j * LDBk + k]
+constexpr int kGmLDBj = 64 + 8;    // B, transposed:     Bs[k * LDBj + j]
+constexpr int kGmAStage = 128 * (kGmLDAk > kGmLDAi * 8 ? kGmLDAk : kGmLDAi * 8);  // >= both layouts
+constexpr int kGmAStageD = (kGmKC * kGmLDAk > 128 * kGmLDAi ? kGmKC * kGmLDAk : 128 * kGmLDAi);
+constexpr int kGmBStageD = (64 * kGmLDBk > kGmKC * kGmLDBj ? 64 * kGmLDBk : kGmKC * kGmLDBj);
+constexpr size_t kGmSmem = (size_t)2 * (kGmAStageD + kGmBStageD) * sizeof(double);
 
-template <int NT>
+template <int NT, bool TA, bool TB>
 __global__ void __launch_bounds__(256) gemm_mma_kernel(GemmLaunch g) {
-  __shared__ __align__(16) double As[kGmKC * kGmLDA];
-  __shared__ __align__(16) double Bs[8 * NT * kGmLDB];
+  extern __shared__ __align__(16) double gsm[];
+  double* As0 = gsm;
+  double* Bs0 = gsm + 2 * kGmAStageD;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, gq = lane >> 2, t = lane & 3;
   const int i0 = warp * 16;
+  const int nk = (g.K + kGmKC - 1) / kGmKC;
   for (int64_t b = blockIdx.x; b < g.batch; b += gridDim.x) {
     const double* A = (const double*)g.a + b * g.a_stride;
     const double* B = (const double*)g.b + b * g.b_stride;
     double* C = (double*)g.c + b * g.c_stride;
+    auto stage = [&](int buf, int k0) {
+      double* As = As0 + buf * kGmAStageD;
+      double* Bs = Bs0 + buf * kGmBStageD;
+      if (!TA) {  // A column-major M x K: 2 consecutive rows i per 16 B
+        for (int e = tid; e < kGmKC * 64; e += 256) {
+          const int kk = e >> 6, ii = 2 * (e & 63), gk = k0 + kk;
+          const bool ok = ii < g.M && gk < g.K;
+          cpa16z(&As[kk * kGmLDAk + ii], ok ? A + (size_t)gk * g.lda + ii : A, ok);
+        }
+      } else {  // A stored K x M: 2 consecutive k per 16 B
+        for (int e = tid; e < 128 * (kGmKC / 2); e += 256) {
+          const int ii = e / (kGmKC / 2), kk = 2 * (e % (kGmKC / 2)), gk = k0 + kk;
+          const bool ok = ii < g.M && gk < g.K;
+          cpa16z(&As[ii * kGmLDAi + kk], ok ? A + (size_t)ii * g.lda + gk : A, ok);
+        }
+      }
+      if (!TB) {  // B column-major K x N: 2 consecutive k per 16 B
+        for (int e = tid; e < 8 * NT * (kGmKC / 2); e += 256) {
+          const int jj = e / (kGmKC / 2), kk = 2 * (e % (kGmKC / 2)), gk = k0 + kk;
+          const bool ok = jj < g.N && gk < g.K;
+          cpa16z(&Bs[jj * kGmLDBk + kk], ok ? B + (size_t)jj * g.ldb + gk : B, ok);
+        }
+      } else {  // B stored N x K (row-major K x N): 2 consecutive j per 16 B
+        for (int e = tid; e < kGmKC * 4 * NT; e += 256) {
+          const int kk = e / (4 * NT), jj = 2 * (e % (4 * NT)), gk = k0 + kk;
+          const bool ok = jj < g.N && gk < g.K;
+          cpa16z(&Bs[kk * kGmLDBj + jj], ok ? B + (size_t)gk * g.ldb + jj : B, ok);
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
     double acc[2][NT][2];
 #pragma unroll
     for (int x = 0; x < 2; ++x)
 #pragma unroll
       for (int y = 0; y < NT; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
-    for (int k0 = 0; k0 < g.K; k0 += kGmKC) {
-      __syncthreads();
-      if (!g.ta) {  // A column-major M x K: rows contiguous
-        for (int e = tid; e < kGmKC * 128; e += 256) {
-          const int kk = e >> 7, ii = e & 127, gk = k0 + kk;
-          As[kk * kGmLDA + ii] = (ii < g.M && gk < g.K) ? A[(size_t)gk * g.lda + ii] : 0.0;
-        }
-      } else {  // A stored K x M: k contiguous
-        for (int e = tid; e < kGmKC * 128; e += 256) {
-          const int kk = e % kGmKC, ii = e / kGmKC, gk = k0 + kk;
-          As[kk * kGmLDA + ii] = (ii < g.M && gk < g.K) ? A[(size_t)ii * g.lda + gk] : 0.0;
-        }
-      }
-      if (!g.tb) {  // B column-major K x N: k contiguous
-        for (int e = tid; e < kGmKC * 8 * NT; e += 256) {
-          const int kk = e % kGmKC, jj = e / kGmKC, gk = k0 + kk;
-          Bs[jj * kGmLDB + kk] = (jj < g.N && gk < g.K) ? B[(size_t)jj * g.ldb + gk] : 0.0;
-        }
-      } else {  // B stored N x K: j contiguous
-        for (int e = tid; e < kGmKC * 8 * NT; e += 256) {
-          const int jj = e % (8 * NT), kk = e / (8 * NT), gk = k0 + kk;
-          Bs[jj * kGmLDB + kk] = (jj < g.N && gk < g.K) ? B[(size_t)gk * g.ldb + jj] : 0.0;
-        }
+    __syncthreads();  // previous matrix done with the stages
+    stage(0, 0);
+    for (int kc = 0; kc < nk; ++kc) {
+      if (kc + 1 < nk) {
+        stage((kc + 1) & 1, (kc + 1) * kGmKC);
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      } else {
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
       }
       __syncthreads();
+      const double* As = As0 + (kc & 1) * kGmAStageD;
+      const double* Bs = Bs0 + (kc & 1) * kGmBStageD;
 #pragma unroll
       for (int kq = 0; kq < kGmKC; kq += 4) {
         double av[2], bv[NT];
 #pragma unroll
-        for (int x = 0; x < 2; ++x) av[x] = As[(kq + t) * kGmLDA + i0 + 8 * x + gq];
+        for (int x = 0; x < 2; ++x)
+          av[x] = TA ? As[(i0 + 8 * x + gq) * kGmLDAi + kq + t] : As[(kq + t) * kGmLDAk + i0 + 8 * x + gq];
 #pragma unroll
-        for (int y = 0; y < NT; ++y) bv[y] = Bs[(8 * y + gq) * kGmLDB + kq + t];
+        for (int y = 0; y < NT; ++y)
+          bv[y] = TB ? Bs[(kq + t) * kGmLDBj + 8 * y + gq] : Bs[(8 * y + gq) * kGmLDBk + kq + t];
 #pragma unroll
         for (int x = 0; x < 2; ++x)
 #pragma unroll
           for (int y = 0; y < NT; ++y) dmma884(acc[x][y], av[x], bv[y]);
       }
+      __syncthreads();  // this stage is refilled two chunks later
     }
 #pragma unroll
     for (int x = 0; x < 2; ++x) {
@@ -151,19 +187,38 @@ __global__ void __launch_bounds__(256) gemm_mma_kernel(GemmLaunch g) {
   }
 }
 
-template <int NT>
-static void launch_gemm_mma(const GemmLaunch& g, cudaStream_t st) {
-  int dev = 0, sms = 148;
+template <int NT, bool TA, bool TB>
+static void launch_gemm_mma_t(const GemmLaunch& g, cudaStream_t st) {
+  cudaFuncSetAttribute(gemm_mma_kernel<NT, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGmSmem);
+  int dev = 0, sms = 148, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int64_t cap = (int64_t)sms * 8;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, gemm_mma_kernel<NT, TA, TB>, 256, kGmSmem);
+  if (per < 1) per = 1;
+  const int64_t cap = (int64_t)sms * per;
   const unsigned grid = (unsigned)(g.batch < cap ? g.batch : cap);
-  gemm_mma_kernel<NT><<<grid, 256, 0, st>>>(g);
+  gemm_mma_kernel<NT, TA, TB><<<grid, 256, kGmSmem, st>>>(g);
+}
+
+template <int NT>
+static void launch_gemm_mma(const GemmLaunch& g, cudaStream_t st) {
+  if (!g.ta && !g.tb) launch_gemm_mma_t<NT, false, false>(g, st);
+  if (!g.ta && g.tb) launch_gemm_mma_t<NT, false, true>(g, st);
+  if (g.ta && !g.tb) launch_gemm_mma_t<NT, true, false>(g, st);
+  if (g.ta && g.tb) launch_gemm_mma_t<NT, true, true>(g, st);
+}
+
+// 16-byte cp.async needs 16-byte aligned rows: even leading dimensions and strides
+static bool gemm_mma_ok(const GemmLaunch& g) {
+  auto even = [](int64_t x) { return (x & 1) == 0; };
+  auto al16 = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  return g.M <= 128 && g.N <= 64 && even(g.lda) && even(g.ldb) && even(g.a_stride) && even(g.b_stride) &&
+         al16(g.a) && al16(g.b);
 }
 
 int launch_gemm(int dtype, const GemmLaunch& g, cudaStream_t st) {
   if (g.batch == 0 || g.M == 0 || g.N == 0) return 0;
-  if (dtype == 0 && g.M <= 128 && g.N <= 64) {
+  if (dtype == 0 && gemm_mma_ok(g)) {
     switch ((g.N + 7) / 8) {
       case 1: launch_gemm_mma<1>(g, st); break;
       case 2: launch_gemm_mma<2>(g, st); break;
