@@ -35,6 +35,20 @@ def as_matrix(a, dtype=None):
     return np.asfortranarray(a)
 
 
+def write_matrix_text(path, a):
+    """Matrix text format of core.py:126-134 (re-exported from cli.py)."""
+    from .cli import write_matrix_text as _w
+
+    return _w(path, a)
+
+
+def read_matrix_text(path, dtype=np.float64):
+    """Matrix text format of core.py:137-147 (re-exported from cli.py)."""
+    from .cli import read_matrix_text as _r
+
+    return _r(path, dtype)
+
+
 def resolve_device(device=None):
     if not torch.cuda.is_available():
         raise _lib.BackendUnavailable("no CUDA device visible; batchfact_b200 has no CPU fallback")
