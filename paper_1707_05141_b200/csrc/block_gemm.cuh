@@ -25,6 +25,7 @@ struct BJGemmArgs {
   const uint8_t* active;
   double* e_sweep;
   double tol;
+  int only_v = 0;  // bj_rot_mma: update the V pair only (direct method)
 };
 
 BF_DEV int bj_pair_col(int c, int k, int bi, int bj) { return c < k ? bi * k + c : bj * k + (c - k); }
@@ -338,7 +339,9 @@ __global__ void __launch_bounds__(256) bj_rot_mma(BJGemmArgs<double> a, int step
   // the chunk sequence runs over W (m rows) then V (n_pad rows)
   double* Wm = a.W + b * (int64_t)m * a.n_pad;
   double* Vm = a.V ? a.V + b * (int64_t)a.n_pad * a.n_pad : nullptr;
-  const int nw_ch = (m + CH - 1) / CH, nv_ch = Vm ? (a.n_pad + CH - 1) / CH : 0, nch = nw_ch + nv_ch;
+  const int nw_ch = a.only_v ? 0 : (m + CH - 1) / CH, nv_ch = Vm ? (a.n_pad + CH - 1) / CH : 0;
+  const int nch = nw_ch + nv_ch;
+  if (nch == 0) return;
   auto where = [&](int ch, double*& M, int& ld, int& rows, int& r0, bool& isw) {
     isw = ch < nw_ch;
     M = isw ? Wm : Vm;

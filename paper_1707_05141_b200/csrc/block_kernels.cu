@@ -239,6 +239,130 @@ __global__ void __launch_bounds__(256) bj_direct_step(BJArgs<T> a, int step) {
   if (a.V) pair_times_rot<T>(a.V + b * (int64_t)a.n_pad * a.n_pad, a.n_pad, a.n_pad, k, bi, bj, Vr, Ur, sig2, false);
 }
 
+// ---- batched direct method (fp64, 2k <= 64): bj_dqr -> register-tier inner SVD of R with V ->
+// bj_dapply (+ bj_rot_mma on the V pair). Same operations as bj_direct_step, with the inner SVD
+// taken out of the per-pair CTA and run batched over all active pairs of the step.
+struct BDArgs {
+  double* P;    // slots x m x kk: the factored pair (reflectors below the diagonal)
+  double* tau;  // slots x kk
+  double* G;    // slots x kk x kk: R (inner SVD input)
+  double* U;    // slots x kk x kk: U_R (sorted)
+  double* S;    // slots x kk: sigma (sorted)
+  uint8_t* pact;
+};
+
+// qr(pair) (blockjacobi.py:136), e = scaled_offdiag(R) (:137), skip e <= tol (:139-140)
+__global__ void __launch_bounds__(256) bj_dqr(BJArgs<double> a, BDArgs d, int step) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int P = a.nb / 2;
+  const int64_t b = blockIdx.x / P;
+  const int pk = blockIdx.x % P;
+  const int64_t slot = blockIdx.x;
+  if (b >= a.batch) return;
+  if (!a.active[b]) {
+    if (threadIdx.x == 0) d.pact[slot] = 0;
+    return;
+  }
+  int bi, bj;
+  rr_pair(a.nb, step, pk, bi, bj);
+  const int k = a.k, kk = 2 * k, m = a.m, tid = threadIdx.x;
+  double* Pm = reinterpret_cast<double*>(smem_raw);  // m x kk
+  double* tau = Pm + (size_t)m * kk;                 // kk
+  double* red = tau + kk;                            // 2
+  const double* Wb = a.W + b * (int64_t)m * a.n_pad;
+  for (int e = tid; e < m * kk; e += blockDim.x) {
+    const int c = e / m, r = e % m;
+    Pm[e] = Wb[(size_t)pair_col(c, k, bi, bj) * m + r];
+  }
+  __syncthreads();
+  qr_factor_cta<double, 4>(Pm, m, m, kk, tau);
+  double* G = d.G + slot * kk * kk;
+  for (int e = tid; e < kk * kk; e += blockDim.x) {
+    const int j = e / kk, i = e % kk;
+    G[e] = i <= j ? Pm[(size_t)j * m + i] : 0.0;
+  }
+  double* Pg = d.P + slot * (int64_t)m * kk;
+  for (int e = tid; e < m * kk; e += blockDim.x) Pg[e] = Pm[e];
+  if (tid < kk) d.tau[slot * kk + tid] = tau[tid];
+  __syncthreads();
+  // scaled_offdiag of R (read back from the smem copy: rows < kk of Pm, upper triangle)
+  double best = 0.0;
+  for (int e = tid; e < kk * kk; e += blockDim.x) {
+    const int j = e / kk, i = e % kk;
+    if (i == j) continue;
+    const double gij = i <= j ? Pm[(size_t)j * m + i] : 0.0;
+    const double den = sqrt(fabs(Pm[(size_t)i * m + i])) * sqrt(fabs(Pm[(size_t)j * m + j]));
+    const double num = fabs(gij);
+    const double rt = den > 0.0 ? num / den : (num > 0.0 ? __longlong_as_double(0x7ff0000000000000LL) : 0.0);
+    best = rt > best ? rt : best;
+  }
+  best = warp_allreduce_max(best);
+  if (tid == 0) red[0] = 0.0;
+  __syncthreads();
+  if ((tid & 31) == 0 && best > 0.0) atomic_max_pos(red, best);
+  __syncthreads();
+  if (tid == 0) {
+    atomic_max_pos(a.e_sweep + b, red[0]);
+    d.pact[slot] = red[0] > a.tol ? 1 : 0;
+  }
+}
+
+// new pair = H_0 ... H_{kk-1} [U_R diag(sigma); 0] (== (Q @ U_R) * sigma, blockjacobi.py:143)
+__global__ void __launch_bounds__(256) bj_dapply(BJArgs<double> a, BDArgs d, int step) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int VB = 8;  // reflectors staged per block
+  const int P = a.nb / 2;
+  const int64_t b = blockIdx.x / P;
+  const int pk = blockIdx.x % P;
+  const int64_t slot = blockIdx.x;
+  if (b >= a.batch || !d.pact[slot]) return;
+  int bi, bj;
+  rr_pair(a.nb, step, pk, bi, bj);
+  const int k = a.k, kk = 2 * k, m = a.m, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* X = reinterpret_cast<double*>(smem_raw);  // m x kk
+  double* Vs = X + (size_t)m * kk;                  // VB x m reflector block
+  const double* U = d.U + slot * kk * kk;
+  const double* S = d.S + slot * kk;
+  const double* Pg = d.P + slot * (int64_t)m * kk;
+  const double* tau = d.tau + slot * kk;
+  for (int e = tid; e < m * kk; e += blockDim.x) {
+    const int c = e / m, r = e % m;
+    X[e] = r < kk ? U[(size_t)c * kk + r] * S[c] : 0.0;
+  }
+  for (int j0 = ((kk - 1) / VB) * VB; j0 >= 0; j0 -= VB) {
+    __syncthreads();
+    for (int e = tid; e < VB * m; e += blockDim.x) {
+      const int q = e / m, r = e % m, j = j0 + q;
+      Vs[e] = j < kk ? Pg[(size_t)j * m + r] : 0.0;
+    }
+    __syncthreads();
+    for (int q = VB - 1; q >= 0; --q) {
+      const int j = j0 + q;
+      if (j >= kk) continue;
+      const double tj = tau[j];
+      if (tj != 0.0) {
+        const double* v = Vs + (size_t)q * m;
+        for (int c = warp; c < kk; c += 8) {
+          double* col = X + (size_t)c * m;
+          double s = 0.0;
+          for (int i = j + 1 + lane; i < m; i += 32) s = fma(v[i], col[i], s);
+          s = warp_allreduce_sum(s);
+          const double w = (col[j] + s) * tj;
+          __syncwarp();
+          for (int i = j + 1 + lane; i < m; i += 32) col[i] = fma(-v[i], w, col[i]);
+          if (lane == 0) col[j] -= w;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  double* Wb = a.W + b * (int64_t)m * a.n_pad;
+  for (int e = tid; e < m * kk; e += blockDim.x) {
+    const int c = e / m, r = e % m;
+    Wb[(size_t)pair_col(c, k, bi, bj) * m + r] = X[e];
+  }
+}
+
 template <typename T>
 __global__ void bj_init(BJArgs<T> a, const T* A) {
   const int64_t b = blockIdx.x;
@@ -311,8 +435,15 @@ static size_t direct_smem(int m, int kk, bool p_in) {
 
 template <typename T>
 struct BJLayout {
-  size_t w, v, p, e, act, cand, g, u, s, pact, iws, total;
+  size_t w, v, p, e, act, cand, g, u, s, pact, iws, dp, dtau, dvr, total;
 };
+
+// batched direct pipeline: fp64, 2k in {16, 32, 48, 64} (register-tier inner SVD with V), the
+// pair plus the reflector stage fitting one CTA's shared memory
+static bool bj_batched_direct(int method, int m, int kk, bool f64) {
+  return f64 && method == 1 && kk == 64 &&
+         (size_t)m * kk * 8 + (size_t)8 * m * 8 + 64 * 8 <= 200 * 1024;
+}
 
 // batched Gram pipeline (bj_gram -> register-tier inner SVD -> bj_rot) covers 2k in {16,32,48,64}
 static bool bj_batched_gram(int method, int kk) { return method == 0 && kk % 16 == 0 && kk <= 64; }
@@ -340,16 +471,24 @@ static BJLayout<T> bj_layout(int64_t batch, int m, int n, int bw, int method, bo
   const int kk = 2 * k;
   const int64_t slots = batch * (nb / 2);
   const bool bg = bj_batched_gram(method, kk);
+  const bool bd = bj_batched_direct(method, m, kk, sizeof(T) == 8);
+  const bool bt = bg || bd;
   L.g = off;
-  off += bg ? al((size_t)slots * kk * kk * sizeof(T)) : 0;
+  off += bt ? al((size_t)slots * kk * kk * sizeof(T)) : 0;
   L.u = off;
-  off += bg ? al((size_t)slots * kk * kk * sizeof(T)) : 0;
+  off += bt ? al((size_t)slots * kk * kk * sizeof(T)) : 0;
   L.s = off;
-  off += bg ? al((size_t)slots * kk * sizeof(T)) : 0;
+  off += bt ? al((size_t)slots * kk * sizeof(T)) : 0;
   L.pact = off;
-  off += bg ? al((size_t)slots) : 0;
+  off += bt ? al((size_t)slots) : 0;
+  L.dp = off;
+  off += bd ? al((size_t)slots * m * kk * sizeof(T)) : 0;
+  L.dtau = off;
+  off += bd ? al((size_t)slots * kk * sizeof(T)) : 0;
+  L.dvr = off;
+  off += bd ? al((size_t)slots * kk * kk * sizeof(T)) : 0;
   L.iws = off;
-  off += bg ? al(svd_global_ws_bytes(sizeof(T) == 8 ? 0 : 1, slots, kk, kk, 1, false, 0, 30)) : 0;
+  off += bt ? al(svd_global_ws_bytes(sizeof(T) == 8 ? 0 : 1, slots, kk, kk, 1, bd, 0, 30)) : 0;
   L.total = off;
   return L;
 }
@@ -454,11 +593,70 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
       e = cudaFuncSetAttribute(bj_rot_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRotSmem);
     if (e != cudaSuccess) return (int)e;
   }
+  // batched direct pipeline (fp64, 2k = 64)
+  const bool bd = bj_batched_direct(L.method, L.m, kk, sizeof(T) == 8);
+  BDArgs dd{};
+  BJGemmArgs<T> gv{};
+  size_t dqr_smem = 0, dap_smem = 0;
+  if (bd) {
+    dd.P = (double*)(base + lay.dp);
+    dd.tau = (double*)(base + lay.dtau);
+    dd.G = (double*)(base + lay.g);
+    dd.U = (double*)(base + lay.u);
+    dd.S = (double*)(base + lay.s);
+    dd.pact = (uint8_t*)(base + lay.pact);
+    // inner SVD of every active R: round robin with V (blockjacobi.py:141)
+    in.batch = L.batch * (nb / 2);
+    in.m = kk;
+    in.n = kk;
+    in.a = dd.G;
+    in.a_stride = (int64_t)kk * kk;
+    in.u = dd.U;
+    in.u_stride = (int64_t)kk * kk;
+    in.s = dd.S;
+    in.s_stride = kk;
+    in.v = base + lay.dvr;
+    in.v_stride = (int64_t)kk * kk;
+    in.sweeps = nullptr;
+    in.converged = nullptr;
+    in.rotations = nullptr;
+    in.tol = a.tol_inner;
+    in.max_sweeps = 30;
+    in.ordering = 1;
+    in.tier = 0;
+    in.transpose_a = false;
+    in.active = dd.pact;
+    // V pair <- V pair @ V_R on the FP64 tensor cores (blockjacobi.py:146-149)
+    gv.batch = L.batch;
+    gv.m = L.m;
+    gv.n_pad = np;
+    gv.k = k;
+    gv.nb = nb;
+    gv.W = a.W;
+    gv.V = a.V;
+    gv.U = (T*)(base + lay.dvr);
+    gv.S = (T*)dd.S;
+    gv.pair_act = dd.pact;
+    gv.active = a.active;
+    gv.only_v = 1;
+    dqr_smem = ((size_t)L.m * kk + kk + 2) * sizeof(double);
+    dap_smem = ((size_t)L.m * kk + (size_t)8 * L.m) * sizeof(double);
+    e = cudaFuncSetAttribute(bj_dqr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dqr_smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(bj_dapply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dap_smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(bj_rot_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRotSmem);
+    if (e != cudaSuccess) return (int)e;
+  }
   void* iws = base + lay.iws;
   const size_t iws_bytes = lay.total - lay.iws;
   for (int sw = 0; sw < L.max_sweeps; ++sw) {
     for (int s = 0; s < nb - 1; ++s) {
-      if (bg) {
+      if (bd) {
+        bj_dqr<<<grid, 256, dqr_smem, st>>>(*reinterpret_cast<BJArgs<double>*>(&a), dd, s);
+        int rc = launch_svd(0, in, iws, iws_bytes, st);
+        if (rc) return rc;
+        bj_dapply<<<grid, 256, dap_smem, st>>>(*reinterpret_cast<BJArgs<double>*>(&a), dd, s);
+        if (a.V) bj_rot_mma<<<grid, 256, kRotSmem, st>>>(*reinterpret_cast<BJGemmArgs<double>*>(&gv), s);
+      } else if (bg) {
         const int TT = kk / 16;
         if (TT == 1) bj_gram<T, 1><<<grid, 256, 0, st>>>(g, s);
         if (TT == 2) bj_gram<T, 2><<<grid, 256, 0, st>>>(g, s);

@@ -1,1 +1,2 @@
-for v in base new base new; do echo "== $v"; BATCHFACT_B200_LIB=build_var/lib_$v.so python tools/time_variants.py 2>&1 | grep "tier=auto" | grep -v serial | grep -v "32x32"; done
+timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "block" 2>&1 | tail -3
+python tools/time_block.py
