@@ -307,10 +307,31 @@ __global__ void __launch_bounds__(256) bj_dqr(BJArgs<double> a, BDArgs d, int st
   }
 }
 
-// new pair = H_0 ... H_{kk-1} [U_R diag(sigma); 0] (== (Q @ U_R) * sigma, blockjacobi.py:143)
-__global__ void __launch_bounds__(256) bj_dapply(BJArgs<double> a, BDArgs d, int step) {
+// new pair = H_0 ... H_{kk-1} [U_R diag(sigma); 0] (== (Q @ U_R) * sigma, blockjacobi.py:143).
+// Same product in compact-WY form on the FP64 tensor cores: with the reflectors Y (unit lower
+// trapezoidal, m x 64) and tau, H_0 ... H_63 = I - Y T Y^T (LAPACK dlarft, forward / columnwise:
+// T_jj = tau_j, T[0:j, j] = -tau_j T[0:j, 0:j] (Y^T Y)[0:j, j]), so the new pair
+// Q [X1; 0] = [X1; 0] - Y (T (Y1^T X1)) with X1 = U_R diag(sigma) and Y1 the top 64 rows of Y.
+// Every product is a 64-wide DMMA GEMM (warp w: a 16 x 32 block of the 64 x 64 output).
+constexpr int kWyLD = 64 + 4;   // 64 x 64 smem matrices: element (r, c) at [c * LD + r]
+constexpr int kWyCH = 32;       // Y rows per staged chunk
+constexpr int kWyLDY = 64 + 4;  // Y chunk: element (r, c) at [r * LDY + c] (row-major)
+constexpr size_t kWySmem = (size_t)(3 * 64 * kWyLD + kWyCH * kWyLDY + 64) * sizeof(double);
+
+BF_DEV void wy_dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+// Y[r][c] of the factored pair: 1 on the diagonal, the stored reflector below, 0 above
+BF_DEV double wy_y(const double* Pg, int m, int r, int c) {
+  return r > c ? Pg[(size_t)c * m + r] : (r == c ? 1.0 : 0.0);
+}
+
+__global__ void __launch_bounds__(256) bj_dapply_wy(BJArgs<double> a, BDArgs d, int step) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int VB = 8;  // reflectors staged per block
+  constexpr int KK = 64, LD = kWyLD, LDY = kWyLDY, CH = kWyCH;
   const int P = a.nb / 2;
   const int64_t b = blockIdx.x / P;
   const int pk = blockIdx.x % P;
@@ -318,48 +339,160 @@ __global__ void __launch_bounds__(256) bj_dapply(BJArgs<double> a, BDArgs d, int
   if (b >= a.batch || !d.pact[slot]) return;
   int bi, bj;
   rr_pair(a.nb, step, pk, bi, bj);
-  const int k = a.k, kk = 2 * k, m = a.m, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* X = reinterpret_cast<double*>(smem_raw);  // m x kk
-  double* Vs = X + (size_t)m * kk;                  // VB x m reflector block
-  const double* U = d.U + slot * kk * kk;
-  const double* S = d.S + slot * kk;
-  const double* Pg = d.P + slot * (int64_t)m * kk;
-  const double* tau = d.tau + slot * kk;
-  for (int e = tid; e < m * kk; e += blockDim.x) {
-    const int c = e / m, r = e % m;
-    X[e] = r < kk ? U[(size_t)c * kk + r] * S[c] : 0.0;
-  }
-  for (int j0 = ((kk - 1) / VB) * VB; j0 >= 0; j0 -= VB) {
+  const int k = a.k, m = a.m, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int r0 = (warp >> 1) * 16, c0 = (warp & 1) * 32;  // this warp's 16 x 32 output block
+  double* bufA = reinterpret_cast<double*>(smem_raw);
+  double* bufB = bufA + 64 * LD;
+  double* bufC = bufB + 64 * LD;
+  double* Ys = bufC + 64 * LD;  // CH x LDY
+  double* taus = Ys + CH * LDY;
+  const double* Pg = d.P + slot * (int64_t)m * KK;
+  const double* U = d.U + slot * KK * KK;
+  const double* S = d.S + slot * KK;
+  if (tid < KK) taus[tid] = d.tau[slot * KK + tid];
+  double acc[2][4][2];
+  auto zero = [&]() {
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  };
+  auto store = [&](double* M) {  // fragments -> M (column-major 64 x 64, ld LD)
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) M[(c0 + 8 * y + 2 * t + q) * LD + r0 + 8 * x + g] = acc[x][y][q];
+  };
+  // ---- G_Y = Y^T Y (accumulated over row chunks of Y)
+  zero();
+  for (int rc = 0; rc < m; rc += CH) {
     __syncthreads();
-    for (int e = tid; e < VB * m; e += blockDim.x) {
-      const int q = e / m, r = e % m, j = j0 + q;
-      Vs[e] = j < kk ? Pg[(size_t)j * m + r] : 0.0;
+    for (int e = tid; e < CH * KK; e += 256) {
+      const int rr = e / KK, c = e % KK, r = rc + rr;
+      Ys[rr * LDY + c] = r < m ? wy_y(Pg, m, r, c) : 0.0;
     }
     __syncthreads();
-    for (int q = VB - 1; q >= 0; --q) {
-      const int j = j0 + q;
-      if (j >= kk) continue;
-      const double tj = tau[j];
-      if (tj != 0.0) {
-        const double* v = Vs + (size_t)q * m;
-        for (int c = warp; c < kk; c += 8) {
-          double* col = X + (size_t)c * m;
-          double s = 0.0;
-          for (int i = j + 1 + lane; i < m; i += 32) s = fma(v[i], col[i], s);
-          s = warp_allreduce_sum(s);
-          const double w = (col[j] + s) * tj;
-          __syncwarp();
-          for (int i = j + 1 + lane; i < m; i += 32) col[i] = fma(-v[i], w, col[i]);
-          if (lane == 0) col[j] -= w;
-        }
+#pragma unroll
+    for (int k0 = 0; k0 < CH; k0 += 4) {
+      double av[2], bv[4];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) av[x] = Ys[(k0 + t) * LDY + r0 + 8 * x + g];  // A[i][k] = Y[k][i]
+#pragma unroll
+      for (int y = 0; y < 4; ++y) bv[y] = Ys[(k0 + t) * LDY + c0 + 8 * y + g];  // B[k][j] = Y[k][j]
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) wy_dmma(acc[x][y], av[x], bv[y]);
+    }
+  }
+  store(bufA);  // G_Y
+  // ---- X1 = U_R diag(sigma) -> bufC
+  for (int e = tid; e < KK * KK; e += 256) {
+    const int c = e / KK, r = e % KK;
+    bufC[c * LD + r] = U[(size_t)c * KK + r] * S[c];
+  }
+  __syncthreads();
+  // ---- T (upper triangular) -> bufB, column by column
+  for (int j = 0; j < KK; ++j) {
+    if (tid < KK) {
+      const int i = tid;
+      double v = 0.0;
+      if (i < j) {
+        double z = 0.0;
+        for (int l = i; l < j; ++l) z = fma(bufB[l * LD + i], bufA[j * LD + l], z);
+        v = -taus[j] * z;
+      } else if (i == j) {
+        v = taus[j];
+      }
+      bufB[j * LD + i] = v;
+    }
+    __syncthreads();
+  }
+  // ---- W1 = Y1^T X1 (Y1 = top 64 rows of Y) -> bufA
+  zero();
+  for (int rc = 0; rc < KK; rc += CH) {
+    for (int e = tid; e < CH * KK; e += 256) {
+      const int rr = e / KK, c = e % KK, r = rc + rr;
+      Ys[rr * LDY + c] = wy_y(Pg, m, r, c);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k0 = 0; k0 < CH; k0 += 4) {
+      double av[2], bv[4];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) av[x] = Ys[(k0 + t) * LDY + r0 + 8 * x + g];               // Y1[k][i]
+#pragma unroll
+      for (int y = 0; y < 4; ++y) bv[y] = bufC[(c0 + 8 * y + g) * LD + rc + k0 + t];       // X1[k][j]
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) wy_dmma(acc[x][y], av[x], bv[y]);
+    }
+    __syncthreads();
+  }
+  store(bufA);  // W1 (G_Y no longer needed)
+  __syncthreads();
+  // ---- W2 = T W1 -> bufC (X1 is re-read from U, S below)
+  zero();
+#pragma unroll 4
+  for (int k0 = 0; k0 < KK; k0 += 4) {
+    double av[2], bv[4];
+#pragma unroll
+    for (int x = 0; x < 2; ++x) av[x] = bufB[(k0 + t) * LD + r0 + 8 * x + g];  // T[i][k]
+#pragma unroll
+    for (int y = 0; y < 4; ++y) bv[y] = bufA[(c0 + 8 * y + g) * LD + k0 + t];  // W1[k][j]
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) wy_dmma(acc[x][y], av[x], bv[y]);
+  }
+  __syncthreads();
+  store(bufC);
+  // ---- new pair = [X1; 0] - Y W2, 64-row chunks of Y, written straight to W
+  double* Wb = a.W + b * (int64_t)m * a.n_pad;
+  for (int rc = 0; rc < m; rc += 64) {
+    zero();
+    for (int half = 0; half < 64; half += CH) {
+      __syncthreads();
+      for (int e = tid; e < CH * KK; e += 256) {
+        const int rr = e / KK, c = e % KK, r = rc + half + rr;
+        Ys[rr * LDY + c] = r < m ? wy_y(Pg, m, r, c) : 0.0;
       }
       __syncthreads();
+      // rows r0..r0+15 of this 64-row chunk live in the half that contains them
+      if ((r0 >= half) && (r0 < half + CH)) {
+        const int rl = r0 - half;
+#pragma unroll 4
+        for (int k0 = 0; k0 < KK; k0 += 4) {
+          double av[2], bv[4];
+#pragma unroll
+          for (int x = 0; x < 2; ++x) av[x] = Ys[(rl + 8 * x + g) * LDY + k0 + t];  // Y[i][k]
+#pragma unroll
+          for (int y = 0; y < 4; ++y) bv[y] = bufC[(c0 + 8 * y + g) * LD + k0 + t];  // W2[k][j]
+#pragma unroll
+          for (int x = 0; x < 2; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) wy_dmma(acc[x][y], av[x], bv[y]);
+        }
+      }
     }
-  }
-  double* Wb = a.W + b * (int64_t)m * a.n_pad;
-  for (int e = tid; e < m * kk; e += blockDim.x) {
-    const int c = e / m, r = e % m;
-    Wb[(size_t)pair_col(c, k, bi, bj) * m + r] = X[e];
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      const int r = rc + r0 + 8 * x + g;
+      if (r < m) {
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int c = c0 + 8 * y + 2 * t + q;
+            const double x1 = r < KK ? U[(size_t)c * KK + r] * S[c] : 0.0;
+            Wb[(size_t)pair_col(c, k, bi, bj) * m + r] = x1 - acc[x][y][q];
+          }
+      }
+    }
   }
 }
 
@@ -640,9 +773,10 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
     gv.active = a.active;
     gv.only_v = 1;
     dqr_smem = ((size_t)L.m * kk + kk + 2) * sizeof(double);
-    dap_smem = ((size_t)L.m * kk + (size_t)8 * L.m) * sizeof(double);
+    dap_smem = kWySmem;
     e = cudaFuncSetAttribute(bj_dqr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dqr_smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(bj_dapply, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dap_smem);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(bj_dapply_wy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dap_smem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(bj_rot_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRotSmem);
     if (e != cudaSuccess) return (int)e;
   }
@@ -654,7 +788,7 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
         bj_dqr<<<grid, 256, dqr_smem, st>>>(*reinterpret_cast<BJArgs<double>*>(&a), dd, s);
         int rc = launch_svd(0, in, iws, iws_bytes, st);
         if (rc) return rc;
-        bj_dapply<<<grid, 256, dap_smem, st>>>(*reinterpret_cast<BJArgs<double>*>(&a), dd, s);
+        bj_dapply_wy<<<grid, 256, dap_smem, st>>>(*reinterpret_cast<BJArgs<double>*>(&a), dd, s);
         if (a.V) bj_rot_mma<<<grid, 256, kRotSmem, st>>>(*reinterpret_cast<BJGemmArgs<double>*>(&gv), s);
       } else if (bg) {
         const int TT = kk / 16;
