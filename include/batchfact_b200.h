@@ -118,6 +118,19 @@ BF_API int bf_make_matrix_batched_f64(int64_t batch, int32_t m, int32_t n, int32
                                uint64_t seed_lo, uint64_t seed_hi, int64_t index_base, double* a, double* sigma,
                                void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- strided batched GEMM, C_b = op(A_b) op(B_b) (column-major; op = transpose when t* != 0).
+ * The batched matrix-matrix products of the H^2 compression ("After forming the TE
+ * matrices using batched matrix-matrix multiplication"; "S~_ts = T_t S_ts T_s^T using
+ * batched matrix-matrix multiplications"). op(A) is M x K, op(B) is K x N, C is M x N (ldc >= M).
+ * f64 runs on the FP64 tensor cores (DMMA) when M <= 128, N <= 64 and the operands are 16-byte
+ * aligned with even leading dimensions/strides; otherwise a tiled CUDA-core kernel. */
+BF_API int bf_gemm_batched_f64(int64_t batch, int32_t M, int32_t N, int32_t K, const double* a, int32_t lda,
+                        int64_t a_stride, int32_t ta, const double* b, int32_t ldb, int64_t b_stride, int32_t tb,
+                        double* c, int32_t ldc, int64_t c_stride, void* stream);
+BF_API int bf_gemm_batched_f32(int64_t batch, int32_t M, int32_t N, int32_t K, const float* a, int32_t lda,
+                        int64_t a_stride, int32_t ta, const float* b, int32_t ldb, int64_t b_stride, int32_t tb,
+                        float* c, int32_t ldc, int64_t c_stride, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

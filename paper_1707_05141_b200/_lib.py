@@ -48,6 +48,8 @@ BF_ERR_UNSUPPORTED = -3
 
 # every symbol include/batchfact_b200.h declares
 EXPORTS = (
+    "bf_gemm_batched_f64",
+    "bf_gemm_batched_f32",
     "bf_last_error",
     "bf_version",
     "bf_qr_workspace_size",
@@ -124,6 +126,10 @@ def load():
     L.bf_make_matrix_workspace_size.restype = SZ
     L.bf_make_matrix_batched_f64.argtypes = [I64, I32, I32, I32, D, I32, U64, U64, I64, P, P, P, SZ, P]
     L.bf_make_matrix_batched_f64.restype = ctypes.c_int
+    for name in ("bf_gemm_batched_f64", "bf_gemm_batched_f32"):
+        f = getattr(L, name)
+        f.argtypes = [I64, I32, I32, I32, P, I32, I64, I32, P, I32, I64, I32, P, I32, I64, P]
+        f.restype = ctypes.c_int
     _lib = L
     return L
 

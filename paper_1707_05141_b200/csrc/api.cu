@@ -268,6 +268,40 @@ int rsvd_impl(int64_t batch, int m, int n, int k, int p, uint64_t slo, uint64_t 
   return BF_OK;
 }
 
+template <typename T>
+int gemm_impl(int64_t batch, int M, int N, int K, const T* a, int lda, int64_t as, int ta, const T* b, int ldb,
+              int64_t bs, int tb, T* c, int ldc, int64_t cs, void* st) {
+  if (batch < 0 || M < 0 || N < 0 || K < 0) return fail(BF_ERR_ARG, "negative batch or shape");
+  if (ldc < std::max(M, 1)) return fail(BF_ERR_ARG, "ldc %d < M %d", ldc, M);
+  if (lda < std::max(ta ? K : M, 1)) return fail(BF_ERR_ARG, "lda %d too small", lda);
+  if (ldb < std::max(tb ? N : K, 1)) return fail(BF_ERR_ARG, "ldb %d too small", ldb);
+  if (batch == 0 || M == 0 || N == 0) return BF_OK;
+  if (K == 0) {  // empty inner dimension: C = 0
+    if (ldc == M && cs == (int64_t)M * N)
+      cudaMemsetAsync(c, 0, sizeof(T) * (size_t)batch * M * N, S(st));
+    else
+      for (int64_t i = 0; i < batch; ++i) cudaMemset2DAsync(c + i * cs, sizeof(T) * ldc, 0, sizeof(T) * M, N, S(st));
+    return cuda_rc((int)cudaGetLastError(), "gemm");
+  }
+  bf::GemmLaunch g;
+  g.batch = batch;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.a = a;
+  g.lda = lda;
+  g.a_stride = as;
+  g.ta = ta != 0;
+  g.b = b;
+  g.ldb = ldb;
+  g.b_stride = bs;
+  g.tb = tb != 0;
+  g.c = c;
+  g.ldc = ldc;
+  g.c_stride = cs;
+  return cuda_rc(bf::launch_gemm(sizeof(T) == 8 ? 0 : 1, g, S(st)), "gemm");
+}
+
 }  // namespace
 
 extern "C" {
@@ -394,6 +428,17 @@ int bf_make_matrix_batched_f64(int64_t batch, int32_t m, int32_t n, int32_t mode
   if ((rc = bf::launch_scale_cols_f64(batch, m, n, P, sg, cs))) return cuda_rc(rc, "make_matrix");
   bf::GemmLaunch g{batch, m, n, n, P, m, (int64_t)m * n, false, Qn, n, (int64_t)n * n, true, a, m, (int64_t)m * n};
   return cuda_rc(bf::launch_gemm(0, g, cs), "make_matrix");
+}
+
+int bf_gemm_batched_f64(int64_t batch, int32_t M, int32_t N, int32_t K, const double* a, int32_t lda, int64_t as,
+                        int32_t ta, const double* b, int32_t ldb, int64_t bs, int32_t tb, double* c, int32_t ldc,
+                        int64_t cs, void* st) {
+  return gemm_impl<double>(batch, M, N, K, a, lda, as, ta, b, ldb, bs, tb, c, ldc, cs, st);
+}
+int bf_gemm_batched_f32(int64_t batch, int32_t M, int32_t N, int32_t K, const float* a, int32_t lda, int64_t as,
+                        int32_t ta, const float* b, int32_t ldb, int64_t bs, int32_t tb, float* c, int32_t ldc,
+                        int64_t cs, void* st) {
+  return gemm_impl<float>(batch, M, N, K, a, lda, as, ta, b, ldb, bs, tb, c, ldc, cs, st);
 }
 
 }  // extern "C"

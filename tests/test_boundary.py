@@ -84,3 +84,12 @@ def test_as_matrix_and_batch_error_types():
         bf.as_matrix(np.zeros(3))
     e = bf.BatchError(3, ValueError("x"))
     assert e.index == 3 and "batch entry 3" in str(e)
+
+
+def test_gemm_argument_errors_without_gpu():
+    L = _lib.load()
+    rc = L.bf_gemm_batched_f64(1, 4, 4, 4, None, 2, 16, 0, None, 4, 16, 0, None, 4, 16, None)
+    assert rc == _lib.BF_ERR_ARG and "lda" in _lib.last_error()
+    rc = L.bf_gemm_batched_f64(1, 4, 4, 4, None, 4, 16, 0, None, 4, 16, 0, None, 3, 16, None)
+    assert rc == _lib.BF_ERR_ARG and "ldc" in _lib.last_error()
+    assert L.bf_gemm_batched_f64(0, 4, 4, 4, None, 4, 16, 0, None, 4, 16, 0, None, 4, 16, None) == _lib.BF_OK

@@ -15,7 +15,9 @@ def test_no_arguments_is_usage_exit_1(capsys):
 def test_unknown_flag_is_usage_exit_1(capsys):
     assert cli.main(["bench", "svd", "--bogus", "1"]) == 1
     assert cli.main(["bench"]) == 1
-    assert cli.main(["compress", "--n", "4096"]) == 1
+    assert cli.main(["compress", "--n", "0"]) == 1
+    assert cli.main(["compress", "--eps", "-1"]) == 1
+    assert cli.main(["compress", "--svd", "qr"]) == 1
 
 
 def test_matrix_text_roundtrip(tmp_path):
