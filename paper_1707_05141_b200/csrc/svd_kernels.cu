@@ -28,6 +28,7 @@ struct SvdArgs {
   double tol;
   int max_sweeps, ordering;
   bool in_smem;
+  bool w_in_smem;  // !in_smem: W (+ candidates) still in shared memory, only V in global
   T* gws;  // per-matrix global workspace when !in_smem
   int64_t gws_stride;
   const uint8_t* active;
@@ -54,11 +55,23 @@ __global__ void __launch_bounds__(512) svd_cta_kernel(SvdArgs<T> a) {
   if (a.active && !a.active[b]) return;
   const int m = a.m, n = a.n, nw = a.nw;
   const bool accv = a.v != nullptr;
-  T* base = a.in_smem ? reinterpret_cast<T*>(smem_raw) : a.gws + b * a.gws_stride;
-  T* W = base;
-  T* V = accv ? W + (size_t)m * nw : nullptr;
-  T* cand = W + (size_t)m * nw + (accv ? (size_t)nw * nw : 0);
-  unsigned char* tail = smem_raw + (a.in_smem ? svd_work_elems<T>(m, nw, accv) * sizeof(T) : 0);
+  T* W;
+  T* V;
+  T* cand;
+  size_t smem_elems;
+  if (a.in_smem || !a.w_in_smem) {  // W, V, candidates contiguous, all in smem or all in global
+    T* base = a.in_smem ? reinterpret_cast<T*>(smem_raw) : a.gws + b * a.gws_stride;
+    W = base;
+    V = accv ? W + (size_t)m * nw : nullptr;
+    cand = W + (size_t)m * nw + (accv ? (size_t)nw * nw : 0);
+    smem_elems = a.in_smem ? svd_work_elems<T>(m, nw, accv) : 0;
+  } else {  // W + candidates in smem, V (touched once per rotation) in global / L2
+    W = reinterpret_cast<T*>(smem_raw);
+    cand = W + (size_t)m * nw;
+    V = accv ? a.gws + b * a.gws_stride : nullptr;
+    smem_elems = svd_work_elems<T>(m, nw, false);
+  }
+  unsigned char* tail = smem_raw + smem_elems * sizeof(T);
   T* sig = reinterpret_cast<T*>(tail);
   int* order = reinterpret_cast<int*>(sig + nw);
   int* counters = order + nw;  // 4 ints
@@ -157,7 +170,12 @@ static int launch_svd_t(const SvdLaunch& L, void* ws, cudaStream_t st) {
   a.gws = (T*)ws;
   size_t per = svd_work_elems<T>(L.m, a.nw, accv) * sizeof(T);
   a.gws_stride = (int64_t)(((per + 255) & ~(size_t)255) / sizeof(T));
-  if (!a.in_smem) smem = svd_smem_bytes<T>(L.m, a.nw, accv, false);
+  a.w_in_smem = false;
+  if (!a.in_smem) {
+    const size_t wsm = svd_smem_bytes<T>(L.m, a.nw, false, true);  // W + candidates + tail
+    a.w_in_smem = accv && fits_smem(wsm);
+    smem = a.w_in_smem ? wsm : svd_smem_bytes<T>(L.m, a.nw, accv, false);
+  }
   int pairs = a.nw / 2 > 0 ? a.nw / 2 : 1;
   int nwarps = (pairs + 3) / 4;
   nwarps = nwarps < 2 ? 2 : (nwarps > 16 ? 16 : nwarps);

@@ -570,8 +570,9 @@ def bmm(a, b, *, ta=False, tb=False, out=None):
 
 @dataclass
 class SvdChoice:
-    """Per-node factorisation for the truncation: ``full`` one-sided Jacobi (bf_svd_batched) or
-    ``rsvd`` with a ``samples`` = k + p budget ("randomized SVD with 32 samples")."""
+    """Per-node factorisation for the truncation: ``full`` one-sided Jacobi (bf_svd_batched),
+    ``block`` block Jacobi (direct method) for more than 64 columns, or ``rsvd`` with a
+    ``samples`` = k + p budget ("randomized SVD with 32 samples")."""
 
     kind: str = "full"
     samples: int = 32
@@ -580,23 +581,100 @@ class SvdChoice:
 
 
 def _factor(A, choice, level):
-    """Batched SVD of (B, M, N): returns u (B, M, w), s (B, w) descending, v (B, N, w)."""
+    """Batched SVD of (B, M, N), M >= N: returns u (B, M, w), s (B, w) descending, v (B, N, w).
+
+    ``full``: the one-sided Jacobi tiers (bf_svd_batched: register tier up to 64 columns, else
+    the shared-memory tier); ``block``: block Jacobi, direct method (bf_block_svd_batched, the
+    paper's "direct block Jacobi kernels" for the rank-121 fixture), columns zero-padded to a
+    multiple of the block width; ``rsvd``: bf_rsvd_batched with a k + p = samples budget."""
+    from .blockjacobi import BlockJacobiOptions, block_svd_tensor
     from .jacobi import JacobiOptions, svd_tensor
     from .rsvd import RsvdOptions, rsvd_tensor
 
-    if choice.kind == "full":
-        r = svd_tensor(A, JacobiOptions(ordering="round_robin", accumulate_v=True))
-        return r["u"], r["sigma"], r["v"]
-    w = min(choice.samples, A.shape[2])
-    p = min(choice.oversample, w - 1)
-    r = rsvd_tensor(A, RsvdOptions(k=w - p, p=p, seed=choice.seed + level))
-    return r["u"], r["s"], r["v"]
+    B, M, N = A.shape
+    if choice.kind == "rsvd":
+        w = min(choice.samples, N)
+        p = min(choice.oversample, w - 1)
+        r = rsvd_tensor(A, RsvdOptions(k=w - p, p=p, seed=choice.seed + level))
+        return r["u"], r["s"], r["v"]
+    if choice.kind == "block" and N > 64:
+        bw = 32
+        Np = -(-N // bw) * bw
+        Mp = max(M, Np)
+        Ap = torch.zeros(B, Mp, Np, dtype=A.dtype, device=A.device)
+        Ap[:, :M, :N] = A
+        r = block_svd_tensor(Ap, BlockJacobiOptions(block_width=bw, method="direct", accumulate_v=True))
+        # the padded columns are exactly zero: their sigma are 0 and sort last
+        return r["u"][:, :M, :N], r["sigma"][:, :N], r["v"][:, :N, :N]
+    if M > N and (N > 64 or M > 64):
+        # QR preconditioning (bf_qr_batched): the Jacobi sweeps then run on the N x N triangle,
+        # whose columns fit shared memory; the left vectors are Q U_R (bf_gemm_batched)
+        from .qr import qr_tensor
+
+        q, rr = qr_tensor(A)
+        r = svd_tensor(rr.contiguous(), JacobiOptions(ordering="round_robin", accumulate_v=True))
+        return bmm(q.contiguous(), r["u"].contiguous()), r["sigma"], r["v"]
+    r = svd_tensor(A, JacobiOptions(ordering="round_robin", accumulate_v=True))
+    return r["u"], r["sigma"], r["v"]
+
+
+def _node_svd(A, nz, k, choice, level):
+    """SVD of every node matrix of a level, returned in a common padded form.
+
+    A: (nn, R, k) node matrices with zero rows; nz: (nn, R) bool, the rows that may be nonzero.
+    A node with fewer than k nonzero rows is rank deficient: one-sided Jacobi on it would chase
+    the rounding noise of its null columns forever (the reference's criterion, jacobi.py:145-150,
+    never accepts them), so it is factored as the transpose of its compacted nonzero rows
+    (k x r_i, full column rank) and the roles of the singular vector sets are swapped back.
+    Returns u (nn, R, w), s (nn, w), v (nn, k, w) with w = max width, zero-padded."""
+    nn, R, _ = A.shape
+    dev, dt = A.device, A.dtype
+    cnt = nz.sum(dim=1)
+    cnt_h = cnt.cpu().numpy()
+    wide = np.nonzero(cnt_h < k)[0]
+    tall = np.nonzero(cnt_h >= k)[0]
+    parts = []
+    if len(tall):
+        idx = torch.as_tensor(tall, device=dev)
+        u, s, v = _factor(A[idx], choice, level)
+        parts.append((idx, u, s, v))
+    if len(wide):
+        idx = torch.as_tensor(wide, device=dev)
+        C = int(cnt_h[wide].max())
+        # compacted nonzero rows first (stable), C of them
+        order = torch.argsort((~nz[idx]).to(torch.int8), dim=1, stable=True)[:, :C]  # (b, C)
+        Ac = torch.gather(A[idx], 1, order[:, :, None].expand(-1, -1, k))  # (b, C, k)
+        valid = torch.gather(nz[idx], 1, order)
+        Ac = Ac * valid[:, :, None]
+        if C == 0:
+            ut = torch.zeros(len(wide), k, 0, dtype=dt, device=dev)
+            st = torch.zeros(len(wide), 0, dtype=dt, device=dev)
+            vt = torch.zeros(len(wide), 0, 0, dtype=dt, device=dev)
+        else:
+            ut, st, vt = _factor(Ac.transpose(1, 2).contiguous(), choice, level)  # Ac^T = ut diag(st) vt^T
+        w = st.shape[1]
+        # left vectors of A: vt (C x w) scattered back to the node's row positions
+        uu = torch.zeros(len(wide), R, w, dtype=dt, device=dev)
+        src = vt * valid[:, :, None]
+        uu.scatter_(1, order[:, :, None].expand(-1, -1, w), src)
+        parts.append((idx, uu, st, ut))
+    w = max(p[2].shape[1] for p in parts)
+    U = torch.zeros(nn, R, w, dtype=dt, device=dev)
+    S = torch.zeros(nn, w, dtype=dt, device=dev)
+    V = torch.zeros(nn, k, w, dtype=dt, device=dev)
+    for idx, u, s, v in parts:
+        ww = s.shape[1]
+        U[idx, :, :ww] = u
+        S[idx, :ww] = s
+        V[idx, :, :ww] = v
+    return U, S, V
 
 
 def truncate_basis(H, eps, svd=None):
     """Bottom-up batched-SVD truncation of the basis tree (§8.2).
 
-    Level l is ONE batch: leaves contribute their U (leaf_rows x k_l), inner nodes the stacked
+    Level l is one batched factorisation (two when it mixes full-rank and rank-deficient nodes,
+    see _node_svd): leaves contribute their U (leaf_rows x k_l), inner nodes the stacked
     TE = [T_c1 E_c1; T_c2 E_c2] (2 k~_{l+1} x k_l, formed by bf_gemm_batched). Columns with
     sigma_j >= eps sigma_1 are kept per node (rank floor 1); the level rank is the max and the
     nodes below it get zero columns. New leaf bases / transfer matrices are the kept left vectors
@@ -613,7 +691,9 @@ def truncate_basis(H, eps, svd=None):
     tree = H.tree
     L = tree.num_levels
     rows = H.leaf_rows
+    cnt = torch.as_tensor(tree.hi - tree.lo, device=dev)
     newk = [0] * L
+    keeps = [None] * L
     new_U = [None] * L
     new_E = [None] * L
     T = [None] * L
@@ -622,24 +702,36 @@ def truncate_basis(H, eps, svd=None):
         nn, k = st["nnodes"][l], H.ranks[l]
         inner = l + 1 < L and st["nnodes"][l + 1] > 0
         kc = newk[l + 1] if inner else 0
-        M = max(rows if H.leaf_U[l] is not None else 0, 2 * kc, k)
-        A = torch.zeros(nn, M, k, dtype=dt, device=dev)
+        R = max(rows if H.leaf_U[l] is not None else 0, 2 * kc, 1)
+        A = torch.zeros(nn, R, k, dtype=dt, device=dev)
+        nz = torch.zeros(nn, R, dtype=torch.bool, device=dev)
+        ar = torch.arange(R, device=dev)
         if H.leaf_U[l] is not None:
-            A[st["leafpos"][l], :rows] = H.leaf_U[l]
+            lp = st["leafpos"][l]
+            A[lp, :rows] = H.leaf_U[l]
+            nz[lp] = ar[None, :] < cnt[torch.as_tensor(tree.level_nodes(l), device=dev)[lp]][:, None]
         if inner:
             TE = bmm(T[l + 1], H.transfer[l + 1])  # (nodes at l+1, kc, k)
             pp, sl = st["parentpos"][l + 1], st["slot"][l + 1]
+            kk = keeps[l + 1]
             for j in (0, 1):
                 sel = torch.nonzero(sl == j).flatten()
                 A[pp[sel], j * kc : (j + 1) * kc] = TE[sel]
-        u, s, v = _factor(A, choice, l)
-        s_host = s.double().cpu().numpy()
-        s1 = s_host[:, :1]
-        keep = np.maximum(1, np.sum(s_host >= eps * s1, axis=1)) if s_host.shape[1] else np.ones(nn, np.int64)
-        kl = int(keep.max()) if nn else 1
-        kl = min(kl, s.shape[1])
+                nz[pp[sel], j * kc : (j + 1) * kc] = ar[None, :kc] < kk[sel][:, None]
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        u, s, v = _node_svd(A, nz, k, choice, l)
+        e1.record()
+        s_host = s.double().cpu().numpy()  # the level rank is decided on the host (one small copy)
+        keep = np.maximum(1, np.sum(s_host >= eps * s_host[:, :1], axis=1)) if s_host.shape[1] else np.ones(nn, int)
+        kl = min(int(keep.max()) if nn else 1, s.shape[1]) if s.shape[1] else 1
         newk[l] = kl
-        mask = torch.as_tensor(np.arange(kl)[None, :] < keep[:, None], device=dev, dtype=dt)
+        keeps[l] = torch.as_tensor(np.minimum(keep, kl), device=dev)
+        mask = (torch.arange(kl, device=dev)[None, :] < keeps[l][:, None]).to(dt)
+        if u.shape[2] < kl:  # a 0-width factorisation (all-zero nodes): pad
+            u = torch.nn.functional.pad(u, (0, kl - u.shape[2]))
+            s = torch.nn.functional.pad(s, (0, kl - s.shape[1]))
+            v = torch.nn.functional.pad(v, (0, kl - v.shape[2]))
         Q = u[:, :, :kl] * mask[:, None, :]
         T[l] = ((s[:, :kl] * mask)[:, :, None] * v[:, :, :kl].transpose(1, 2)).contiguous()
         if H.leaf_U[l] is not None:
@@ -651,7 +743,8 @@ def truncate_basis(H, eps, svd=None):
                 sel = torch.nonzero(sl == j).flatten()
                 E[sel] = Q[pp[sel], j * kc : (j + 1) * kc]
             new_E[l + 1] = E
-        info.append(dict(level=l, nodes=nn, rows=M, cols=k, rank_before=k, rank_after=kl,
+        info.append(dict(level=l, nodes=nn, rows=R, cols=k, rank_before=k, rank_after=kl,
+                         svd_ms=round(e0.elapsed_time(e1), 3), wide_nodes=int((nz.sum(1) < k).sum()),
                          node_ranks_max=int(keep.max()) if nn else 0, node_ranks_min=int(keep.min()) if nn else 0))
     return newk, new_U, new_E, T, info[::-1]
 

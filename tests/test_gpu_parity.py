@@ -163,6 +163,23 @@ def test_svd_batch_vs_oracle(shape, tier, ordering):
         assert vec_mismatch(v[b].T, o["v"][b].T, o["s"][b], np.float64) <= 1.0
 
 
+@pytest.mark.parametrize("shape", [(128, 122), (200, 100)])
+def test_svd_shared_tier_v_in_global(shape):
+    """Shapes whose W fits shared memory but W + V does not (W in smem, V in global/L2)."""
+    m, n = shape
+    B = 6
+    a = dev_gauss(B, m, n, 2_000_000 + m + n)
+    r = bf.svd_tensor(a, bf.JacobiOptions(ordering="round_robin", accumulate_v=True))
+    a3 = stack_np(a)
+    o = orc.batch_svd_stacked(a3, m, n, ordering="round_robin", accumulate_v=True, threads=8)
+    s = r["sigma"].cpu().numpy()
+    u, v = stack_np(r["u"]), stack_np(r["v"])
+    for b in range(B):
+        assert sigma_normwise(s[b], o["s"][b]) <= 1e-12
+        assert vec_mismatch(u[b].T, o["u"][b].T, o["s"][b], np.float64) <= 1.0
+        assert vec_mismatch(v[b].T, o["v"][b].T, o["s"][b], np.float64) <= 1.0
+
+
 def test_svd_cfg1_full_batch_properties():
     a = dev_gauss(1000, 32, 32, 1_000_000)
     r = bf.svd_tensor(a, bf.JacobiOptions(ordering="serial", accumulate_v=True))

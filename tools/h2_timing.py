@@ -17,6 +17,8 @@ def main():
     ap.add_argument("--fixtures", default="8:1.0:32,11:2.0:64")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--eps", type=float, default=1e-7)
+    ap.add_argument("--kinds", default="full,rsvd")
+    ap.add_argument("--oracle-max-n", type=int, default=0, help="also time oracle/h2_ref.compress_ref (CPU) up to this n")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     lines = []
@@ -28,7 +30,14 @@ def main():
             H = h2.build_h2(h2.perturbed_grid(n, seed=0), 0.1, order, eta, 64)
             tb = time.perf_counter() - t0
             Hd = H.to("cuda")
-            for kind in ("full", "rsvd"):
+            cpu_s = None
+            if n <= a.oracle_max_n:
+                from oracle import h2_ref
+
+                t0 = time.perf_counter()
+                h2_ref.compress_ref(H, a.eps)
+                cpu_s = time.perf_counter() - t0
+            for kind in a.kinds.split(","):
                 ch = h2.SvdChoice(kind=kind, samples=samples)
                 h2.compress(Hd, a.eps, ch)
                 best = None
@@ -45,7 +54,8 @@ def main():
                            projection_ms=round(rep["projection_ms"], 3), total_ms=round(tot, 3),
                            ranks_before=rep["ranks_before"], ranks_after=rep["ranks_after"], error=err,
                            lowrank_mb_before=round(m0["lowrank"] / 1e6, 3), lowrank_mb_after=round(m1["lowrank"] / 1e6, 3),
-                           dense_mb=round(m0["dense"] / 1e6, 3),
+                           dense_mb=round(m0["dense"] / 1e6, 3), oracle_cpu_s=cpu_s if kind == "full" else None,
+                           level_svd_ms=[lv["svd_ms"] for lv in rep["levels"]],
                            blocks_lowrank=sum(len(g["t"]) for g in H.coupling.values()),
                            blocks_dense=len(H.dense["t"]), levels=H.tree.num_levels)
                 print(json.dumps(rec), flush=True)
