@@ -187,18 +187,24 @@ class GpuConfig:
 
     def kernel_name(self):
         c = self.cfg
-        return {"svd": "svd_reg_kernel", "qr": "qr_reg_kernel", "block": "svd_reg_kernel (inner) + bj_rot + bj_gram",
-                "rsvd": "qr_reg_kernel + svd_reg_kernel + gemm_kernel"}[c["kind"]]
+        if c["kind"] == "svd":
+            return "svd_rr_kernel + svd_rr_vkernel" if c["ordering"] == "round_robin" else "svd_reg_kernel"
+        return {"qr": "qr_reg_kernel", "block": "bj_gram_mma + svd_rr_kernel (inner) + bj_rot_mma",
+                "rsvd": "gemm_mma_kernel + qr_reg_kernel + svd_rr_kernel + svd_rr_vkernel"}[c["kind"]]
 
     def launches_per_step(self):
+        """Our kernels per step, as the ncu launch lists show them (profiles/launches_r01.md)."""
         c = self.cfg
-        if c["kind"] in ("svd", "qr"):
+        if c["kind"] == "svd":
+            return 2 if c["ordering"] == "round_robin" else 1  # sweep kernel + V replay kernel
+        if c["kind"] == "qr":
             return 1
         if c["kind"] == "block":
             nb = c["n"] // 32
-            # init + max_sweeps x (steps x (gram, inner svd, rotation) + finalize) + extract
-            return 1 + 30 * (3 * (nb - 1) + 1) + 1
-        return 9  # rsvd: gaussian, gemm, qr, gemm, qr, svd (+ V replay), gemm, gemm
+            sw = int(self.out["sweeps"].max().item()) if self.out is not None else 30
+            # init + sweeps x (steps x (gram, inner svd, rotation) + finalize)
+            return 1 + sw * (3 * (nb - 1) + 1)
+        return 10  # rsvd: gaussian, 4 DMMA gemms, 2 qr, svd sweep + V replay, sign fix
 
     def flops(self):
         """Algorithmic flops of the last step (counted from the run's own sweep/rotation counters)."""

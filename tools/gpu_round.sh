@@ -14,3 +14,4 @@ bash tools/gpu_ncu_one.sh cfg3_svd_rr_v cfg3 "svd_rr_vkernel"
 bash tools/gpu_ncu_one.sh cfg2_qr_reg2 cfg2 "qr_reg_kernel"
 bash tools/gpu_ncu_one.sh cfg4_bj_rot_mma cfg4 "bj_rot_mma" 3
 bash tools/gpu_ncu_one.sh cfg5_gemm_mma cfg5 "gemm_mma" 1
+PYTHONPATH=. timeout 900 python tools/h2_timing.py --ns 4096,8192,16384,32768 --reps 3 --kinds full,rsvd --oracle-max-n 16384 --out gpurun_out/h2_timing.jsonl > gpurun_out/h2_timing.log 2>&1; echo "h2 rc=$?"
