@@ -360,7 +360,7 @@ def main():
     ap.add_argument("--config", default=HEADLINE, help="headline config (cfg1..cfg5)")
     ap.add_argument("--no-extra", action="store_true", help="skip the other configs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--e2e-chunks", type=int, default=-8, help="host-buffer pipeline chunks for the e2e leg (negative: equal chunks, no taper)")
+    ap.add_argument("--e2e-chunks", type=int, default=-12, help="host-buffer pipeline chunks for the e2e leg (negative: equal chunks, no taper)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
