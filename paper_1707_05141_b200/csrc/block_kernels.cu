@@ -678,6 +678,12 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
   if (e != cudaSuccess) return (int)e;
   const bool bg = bj_batched_gram(L.method, kk);
   BJGemmArgs<T> g;
+  // TMA staging of the DMMA block kernels (bit 0 Gram, bit 1 rotation); BF_BLOCK_TMA overrides
+  static const int tma_sel = [] {
+    const char* e = getenv("BF_BLOCK_TMA");
+    return e ? atoi(e) : kBlockTmaDefault;
+  }();
+  g.tma = tma_sel;
   SvdLaunch in{};
   size_t rot_smem = 0;
   if (bg) {
@@ -730,6 +736,7 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
   const bool bd = bj_batched_direct(L.method, L.m, kk, sizeof(T) == 8);
   BDArgs dd{};
   BJGemmArgs<T> gv{};
+  gv.tma = tma_sel;
   size_t dqr_smem = 0, dap_smem = 0;
   if (bd) {
     dd.P = (double*)(base + lay.dp);
