@@ -307,6 +307,176 @@ __global__ void __launch_bounds__(256) bj_dqr(BJArgs<double> a, BDArgs d, int st
   }
 }
 
+// Register-resident pair QR for m <= 256 (same contract and outputs as bj_dqr): 256 threads,
+// thread r owns row r of the m x 64 pair in registers, the reflector loop unrolled so column
+// indices are compile-time. Per reflector J: the tail norm and alpha (one CTA reduction), the
+// scalars of householder_vector (qr.py:26-48), the dots v . a_c for c = J..63 in one pass (c = J
+// is v . x, giving R_JJ = alpha - tau (v . x) as the reference applies the reflector to its own
+// column, qr.py:84), reduced per warp through a shared-memory transpose and across the 8 warps
+// through a partial-sum row, then the rank-1 update of columns J+1..63. The shared-memory
+// qr_factor_cta it replaces ran each reflector's scalars on one warp while seven waited.
+constexpr int kDqrTS = 65;  // transpose row stride (odd: conflict-free rows and columns)
+constexpr size_t kDqrRegSmem = (size_t)(8 * 32 * kDqrTS + 8 * 64 + 64 + 64 + 32) * sizeof(double);
+
+struct DqrReg {
+  double* tb;    // 8 warps x 32 rows x kDqrTS
+  double* part;  // 8 x 64 warp partial sums
+  double* tot;   // 64: tau * (v . a_c)
+  double* taus;  // 64
+  double* misc;  // 2 x 16 (double-buffered by J parity): [0..7] warp norms, [8] alpha
+  int tid, lane, warp, m;
+
+  template <int J>
+  BF_DEV void col(double (&a)[64]) {
+    const bool live = tid < m;
+    double* ms = misc + 16 * (J & 1);
+    double ts = (tid > J && live) ? a[J] * a[J] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ts += __shfl_xor_sync(0xffffffffu, ts, o);
+    if (lane == 0) ms[warp] = ts;
+    if (tid == J) ms[8] = a[J];
+    __syncthreads();
+    double tail_sq = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) tail_sq += ms[w];
+    const double alpha = ms[8];
+    double tj = 0.0;
+    if (J + 1 < m && tail_sq != 0.0) {  // uniform
+      double beta, denom, rden;
+      householder_scalars(alpha, tail_sq, beta, tj, denom, rden);
+      double v = 0.0, pj = 0.0;
+      if (tid == J) {
+        v = 1.0;
+        pj = alpha;
+      } else if (tid > J && live) {
+        const double x = a[J];
+        v = div_by(x, denom, rden);
+        pj = v * x;
+        a[J] = v;  // reflector stored below the diagonal
+      }
+      constexpr int K = 64 - J;
+      double* row = tb + (warp * 32 + lane) * kDqrTS;
+      row[0] = pj;
+#pragma unroll
+      for (int c = 1; c < K; ++c) row[c] = v * a[J + c];
+      __syncwarp();
+      const double* wt = tb + warp * 32 * kDqrTS;
+      if (lane < K) {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll 8
+        for (int r = 0; r < 32; r += 2) {
+          s0 += wt[r * kDqrTS + lane];
+          s1 += wt[(r + 1) * kDqrTS + lane];
+        }
+        part[warp * 64 + lane] = s0 + s1;
+      }
+      if (lane + 32 < K) {
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll 8
+        for (int r = 0; r < 32; r += 2) {
+          s0 += wt[r * kDqrTS + lane + 32];
+          s1 += wt[(r + 1) * kDqrTS + lane + 32];
+        }
+        part[warp * 64 + lane + 32] = s0 + s1;
+      }
+      __syncthreads();
+      if (tid < K) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) t += part[w * 64 + tid];
+        tot[tid] = t * tj;
+      }
+      __syncthreads();
+      if (tid == J) a[J] = alpha - tot[0];
+#pragma unroll
+      for (int c = 1; c < K; ++c) a[J + c] = fma(-v, tot[c], a[J + c]);
+    }
+    if (tid == 0) taus[J] = tj;
+  }
+
+  template <int J>
+  BF_DEV void from(double (&a)[64]) {
+    if constexpr (J < 64) {
+      col<J>(a);
+      from<J + 1>(a);
+    }
+  }
+};
+
+__global__ void __launch_bounds__(256, 1) bj_dqr_reg(BJArgs<double> a, BDArgs d, int step) {
+  extern __shared__ __align__(16) double dq_smem[];
+  const int P = a.nb / 2;
+  const int64_t b = blockIdx.x / P;
+  const int pk = blockIdx.x % P;
+  const int64_t slot = blockIdx.x;
+  if (b >= a.batch) return;
+  if (!a.active[b]) {
+    if (threadIdx.x == 0) d.pact[slot] = 0;
+    return;
+  }
+  int bi, bj;
+  rr_pair(a.nb, step, pk, bi, bj);
+  const int k = a.k, m = a.m, tid = threadIdx.x;
+  DqrReg q;
+  q.tb = dq_smem;
+  q.part = q.tb + 8 * 32 * kDqrTS;
+  q.tot = q.part + 8 * 64;
+  q.taus = q.tot + 64;
+  q.misc = q.taus + 64;
+  q.tid = tid;
+  q.lane = tid & 31;
+  q.warp = tid >> 5;
+  q.m = m;
+  const double* Wb = a.W + b * (int64_t)m * a.n_pad;
+  double x[64];
+#pragma unroll
+  for (int c = 0; c < 64; ++c) x[c] = tid < m ? Wb[(size_t)pair_col(c, k, bi, bj) * m + tid] : 0.0;
+  q.from<0>(x);
+  // outputs: R (upper triangle, kk x kk) -> G, the factored pair -> P, tau
+  double* G = d.G + slot * 64 * 64;
+  if (tid < 64) {
+#pragma unroll
+    for (int c = 0; c < 64; ++c) G[(size_t)c * 64 + tid] = c >= tid ? x[c] : 0.0;
+  }
+  double* Pg = d.P + slot * (int64_t)m * 64;
+  if (tid < m) {
+#pragma unroll
+    for (int c = 0; c < 64; ++c) Pg[(size_t)c * m + tid] = x[c];
+  }
+  __syncthreads();
+  if (tid < 64) d.tau[slot * 64 + tid] = q.taus[tid];
+  // scaled_offdiag of R (blockjacobi.py:57-76): diagonal to shared memory, row tid vs c > tid
+  double* diag = q.part;  // 64 (free after the loop)
+  double* red = q.tot;
+  if (tid < 64) {
+#pragma unroll
+    for (int c = 0; c < 64; ++c)
+      if (c == tid) diag[c] = x[c];
+  }
+  if (tid == 0) red[0] = 0.0;
+  __syncthreads();
+  double best = 0.0;
+  if (tid < 64) {
+    const double di = sqrt(fabs(diag[tid]));
+#pragma unroll
+    for (int c = 1; c < 64; ++c) {
+      if (c > tid) {
+        const double den = di * sqrt(fabs(diag[c]));
+        const double num = fabs(x[c]);
+        const double rt = den > 0.0 ? num / den : (num > 0.0 ? __longlong_as_double(0x7ff0000000000000LL) : 0.0);
+        best = rt > best ? rt : best;
+      }
+    }
+  }
+  best = warp_allreduce_max(best);
+  if ((tid & 31) == 0 && best > 0.0) atomic_max_pos(red, best);
+  __syncthreads();
+  if (tid == 0) {
+    atomic_max_pos(a.e_sweep + b, red[0]);
+    d.pact[slot] = red[0] > a.tol ? 1 : 0;
+  }
+}
+
 // new pair = H_0 ... H_{kk-1} [U_R diag(sigma); 0] (== (Q @ U_R) * sigma, blockjacobi.py:143).
 // Same product in compact-WY form on the FP64 tensor cores: with the reflectors Y (unit lower
 // trapezoidal, m x 64) and tau, H_0 ... H_63 = I - Y T Y^T (LAPACK dlarft, forward / columnwise:
@@ -738,6 +908,7 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
   BJGemmArgs<T> gv{};
   gv.tma = tma_sel;
   size_t dqr_smem = 0, dap_smem = 0;
+  bool dqr_reg = false;
   if (bd) {
     dd.P = (double*)(base + lay.dp);
     dd.tau = (double*)(base + lay.dtau);
@@ -779,9 +950,11 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
     gv.pair_act = dd.pact;
     gv.active = a.active;
     gv.only_v = 1;
-    dqr_smem = ((size_t)L.m * kk + kk + 2) * sizeof(double);
+    dqr_reg = L.m <= 256;
+    dqr_smem = dqr_reg ? kDqrRegSmem : ((size_t)L.m * kk + kk + 2) * sizeof(double);
     dap_smem = kWySmem;
-    e = cudaFuncSetAttribute(bj_dqr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dqr_smem);
+    e = cudaFuncSetAttribute(dqr_reg ? bj_dqr_reg : bj_dqr, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)dqr_smem);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(bj_dapply_wy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dap_smem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(bj_rot_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRotSmem);
@@ -792,7 +965,10 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
   for (int sw = 0; sw < L.max_sweeps; ++sw) {
     for (int s = 0; s < nb - 1; ++s) {
       if (bd) {
-        bj_dqr<<<grid, 256, dqr_smem, st>>>(*reinterpret_cast<BJArgs<double>*>(&a), dd, s);
+        if (dqr_reg)
+          bj_dqr_reg<<<grid, 256, dqr_smem, st>>>(*reinterpret_cast<BJArgs<double>*>(&a), dd, s);
+        else
+          bj_dqr<<<grid, 256, dqr_smem, st>>>(*reinterpret_cast<BJArgs<double>*>(&a), dd, s);
         int rc = launch_svd(0, in, iws, iws_bytes, st);
         if (rc) return rc;
         bj_dapply_wy<<<grid, 256, dap_smem, st>>>(*reinterpret_cast<BJArgs<double>*>(&a), dd, s);

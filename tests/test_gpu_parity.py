@@ -272,6 +272,28 @@ def test_block_cfg4_gram_vs_oracle():
     assert float(rel.max()) < 1e-12
 
 
+@pytest.mark.parametrize("m,n", [(256, 256), (200, 128), (300, 128)])
+def test_block_direct_bw32_vs_oracle(m, n):
+    """Direct method at the BASELINE block width (pair 2k = 64): register pair QR for m <= 256,
+    shared-memory pair QR above; sigma, vectors, sweeps and flags against the oracle."""
+    B = 4
+    a = dev_gauss(B, m, n, 4_100_000 + m + n)
+    opts = bf.BlockJacobiOptions(method="direct", block_width=32, accumulate_v=True)
+    r = bf.block_svd_tensor(a, opts)
+    o = orc.batch_block_svd_stacked(stack_np(a), m, n, block_width=32, method="direct", tol=1e-13,
+                                    accumulate_v=True, threads=B)
+    s = r["sigma"].cpu().numpy()
+    sw = r["sweeps"].cpu().numpy()
+    cv = r["converged"].cpu().numpy()
+    u, v = stack_np(r["u"]), stack_np(r["v"])
+    for b in range(B):
+        assert sigma_normwise(s[b], o["s"][b]) <= 1e-12
+        assert abs(int(sw[b]) - int(o["sweeps"][b])) <= 1
+        assert bool(cv[b]) == bool(o["converged"][b])
+        assert vec_mismatch(u[b].T, o["u"][b].T, o["s"][b], np.float64) <= 1.0
+        assert vec_mismatch(v[b].T, o["v"][b].T, o["s"][b], np.float64) <= 1.0
+
+
 # ------------------------------------------------------------------ randomized SVD
 
 
