@@ -484,7 +484,7 @@ __global__ void __launch_bounds__(256, 1) bj_dqr_reg(BJArgs<double> a, BDArgs d,
 // Q [X1; 0] = [X1; 0] - Y (T (Y1^T X1)) with X1 = U_R diag(sigma) and Y1 the top 64 rows of Y.
 // Every product is a 64-wide DMMA GEMM (warp w: a 16 x 32 block of the 64 x 64 output).
 constexpr int kWyLD = 64 + 4;   // 64 x 64 smem matrices: element (r, c) at [c * LD + r]
-constexpr int kWyCH = 32;       // Y rows per staged chunk
+constexpr int kWyCH = 64;       // Y rows per staged chunk
 constexpr int kWyLDY = 64 + 4;  // Y chunk: element (r, c) at [r * LDY + c] (row-major)
 constexpr size_t kWySmem = (size_t)(3 * 64 * kWyLD + kWyCH * kWyLDY + 64) * sizeof(double);
 
@@ -540,8 +540,8 @@ __global__ void __launch_bounds__(256) bj_dapply_wy(BJArgs<double> a, BDArgs d, 
   zero();
   for (int rc = 0; rc < m; rc += CH) {
     __syncthreads();
-    for (int e = tid; e < CH * KK; e += 256) {
-      const int rr = e / KK, c = e % KK, r = rc + rr;
+    for (int e = tid; e < CH * KK; e += 256) {  // column-major walk: coalesced reads of Pg
+      const int c = e / CH, rr = e % CH, r = rc + rr;
       Ys[rr * LDY + c] = r < m ? wy_y(Pg, m, r, c) : 0.0;
     }
     __syncthreads();
@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(256) bj_dapply_wy(BJArgs<double> a, BDArgs d, 
   zero();
   for (int rc = 0; rc < KK; rc += CH) {
     for (int e = tid; e < CH * KK; e += 256) {
-      const int rr = e / KK, c = e % KK, r = rc + rr;
+      const int c = e / CH, rr = e % CH, r = rc + rr;
       Ys[rr * LDY + c] = wy_y(Pg, m, r, c);
     }
     __syncthreads();
@@ -628,7 +628,7 @@ __global__ void __launch_bounds__(256) bj_dapply_wy(BJArgs<double> a, BDArgs d, 
     for (int half = 0; half < 64; half += CH) {
       __syncthreads();
       for (int e = tid; e < CH * KK; e += 256) {
-        const int rr = e / KK, c = e % KK, r = rc + half + rr;
+        const int c = e / CH, rr = e % CH, r = rc + half + rr;
         Ys[rr * LDY + c] = r < m ? wy_y(Pg, m, r, c) : 0.0;
       }
       __syncthreads();
