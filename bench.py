@@ -39,10 +39,22 @@ CONFIGS = {
                  desc="batched shared-memory Jacobi SVD, 5,000 random 64x64 fp64 (round_robin, V)"),
     "cfg4": dict(kind="block", m=256, n=256, batch=1000, seed=4_000_000,
                  desc="batched block-Jacobi SVD (gram, bw 32, tol 1e-11, V), 1,000 random 256x256 fp64"),
+    "cfg4d": dict(kind="block", method="direct", m=256, n=256, batch=1000, seed=4_000_000,
+                  desc="batched block-Jacobi SVD, direct method (the reference default: pair QR, inner SVD of R, "
+                       "WY apply; bw 32, tol 1e-13, V), 1,000 random 256x256 fp64"),
     "cfg5": dict(kind="rsvd", m=128, n=128, batch=10_000, seed=5_000_000, k=32, p=8,
                  desc="batched randomized SVD k=32 p=8 of 10,000 128x128 geometric-spectrum (cond 1e16, rank 64) blocks"),
 }
 HEADLINE = "cfg3"
+
+
+def block_opts(c):
+    """cfg4: Gram at tol 1e-11 (BASELINE: tensor-core Gram/rotation); cfg4d: the direct default."""
+    import paper_1707_05141_b200 as bf
+
+    if c.get("method", "gram") == "gram":
+        return bf.BlockJacobiOptions(method="gram", block_width=32, tolerance=1e-11, accumulate_v=True)
+    return bf.BlockJacobiOptions(method="direct", block_width=32, accumulate_v=True)
 
 
 def load_profile(name):
@@ -179,7 +191,7 @@ class GpuConfig:
         elif c["kind"] == "qr":
             self.out = self.k_qr(self.store, m, n, 16)
         elif c["kind"] == "block":
-            opts = bf.BlockJacobiOptions(method="gram", block_width=32, tolerance=1e-11, accumulate_v=True)
+            opts = block_opts(c)
             self.out = self.k_block(self.store, m, n, opts)
         else:
             opts = bf.RsvdOptions(k=c["k"], p=c["p"], seed=5)
@@ -189,6 +201,8 @@ class GpuConfig:
         c = self.cfg
         if c["kind"] == "svd":
             return "svd_rr_kernel + svd_rr_vkernel" if c["ordering"] == "round_robin" else "svd_reg_kernel"
+        if c["kind"] == "block" and c.get("method", "gram") == "direct":
+            return "bj_dqr_reg + svd_rr_kernel + svd_rr_vkernel (inner) + bj_dapply_wy + bj_rot_mma"
         return {"qr": "qr_reg_kernel", "block": "bj_gram_mma + svd_rr_kernel (inner) + bj_rot_mma",
                 "rsvd": "gemm_mma_kernel + qr_reg_kernel + svd_rr_kernel + svd_rr_vkernel"}[c["kind"]]
 
@@ -201,9 +215,11 @@ class GpuConfig:
             return 1
         if c["kind"] == "block":
             nb = c["n"] // 32
-            sw = int(self.out["sweeps"].max().item()) if self.out is not None else 30
-            # init + sweeps x (steps x (gram, inner svd, rotation) + finalize)
-            return 1 + sw * (3 * (nb - 1) + 1)
+            # init + 30 sweeps (launched unconditionally; converged entries exit at once) x (steps x
+            # kernels + finalize) + extract. Gram: gram, inner svd (U only), rotation; direct: pair
+            # QR, inner svd sweep + V replay, WY apply, V-pair rotation
+            per = 3 if c.get("method", "gram") == "gram" else 5
+            return 2 + 30 * (per * (nb - 1) + 1)
         return 10  # rsvd: gaussian, 4 DMMA gemms, 2 qr, svd sweep + V replay, sign fix
 
     def flops(self):
@@ -240,7 +256,7 @@ class GpuConfig:
             def op(x, ib):
                 return list(self.k_qr(x, m, n, 16))
         elif c["kind"] == "block":
-            opts = bf.BlockJacobiOptions(method="gram", block_width=32, tolerance=1e-11, accumulate_v=True)
+            opts = block_opts(c)
 
             def op(x, ib):
                 r = self.k_block(x, m, n, opts)
@@ -323,14 +339,15 @@ def cpu_sample(name, cfg, sample, threads):
     elif cfg["kind"] == "qr":
         orc.batch_qr_stacked(a3, m, n, 16, threads=threads)
     elif cfg["kind"] == "block":
-        orc.batch_block_svd_stacked(a3, m, n, block_width=32, method="gram", tol=1e-11, accumulate_v=True,
-                                    threads=threads)
+        meth = cfg.get("method", "gram")
+        orc.batch_block_svd_stacked(a3, m, n, block_width=32, method=meth, tol=1e-11 if meth == "gram" else 1e-13,
+                                    accumulate_v=True, threads=threads)
     else:
         orc.batch_rsvd_stacked(a3, m, n, cfg["k"], cfg["p"], seed=5, threads=threads)
     return time.perf_counter() - t0
 
 
-CPU_SAMPLE = {"cfg1": 1000, "cfg2": 10_000, "cfg3": 5000, "cfg4": 48, "cfg5": 2000}
+CPU_SAMPLE = {"cfg1": 1000, "cfg2": 10_000, "cfg3": 5000, "cfg4": 48, "cfg4d": 32, "cfg5": 2000}
 
 
 def cpu_baseline(name, cfg, threads, sample=None):
