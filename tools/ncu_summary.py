@@ -40,7 +40,7 @@ STALL_PREFIX2 = "smsp__pcsamp_warps_issue_stalled_"
 
 # capture -> bench config whose dominant kernel it is (later entries win)
 CONFIG_OF = {"cfg1_svd_reg": "cfg1", "cfg2_qr_reg": "cfg2", "cfg3_svd_reg": "cfg3", "cfg4_svd_reg": "cfg4",
-             "cfg5_qr_reg": "cfg5", "cfg3_svd_rr": "cfg3"}
+             "cfg5_qr_reg": "cfg5", "cfg3_svd_rr": "cfg3", "cfg2_qr_reg2": "cfg2", "cfg4d_dqr_reg": "cfg4d"}
 
 
 CONFIG_SUM = {"cfg3": ["cfg3_svd_rr", "cfg3_svd_rr_v"]}
