@@ -483,25 +483,28 @@ __global__ void __launch_bounds__(256, 1) bj_dqr_reg(BJArgs<double> a, BDArgs d,
 // T_jj = tau_j, T[0:j, j] = -tau_j T[0:j, 0:j] (Y^T Y)[0:j, j]), so the new pair
 // Q [X1; 0] = [X1; 0] - Y (T (Y1^T X1)) with X1 = U_R diag(sigma) and Y1 the top 64 rows of Y.
 // Every product is a 64-wide DMMA GEMM (warp w: a 16 x 32 block of the 64 x 64 output).
-constexpr int kWyLD = 64 + 4;   // 64 x 64 smem matrices: element (r, c) at [c * LD + r]
-constexpr int kWyCH = 64;       // Y rows per staged chunk
-constexpr int kWyLDY = 64 + 4;  // Y chunk: element (r, c) at [r * LDY + c] (row-major)
-constexpr size_t kWySmem = (size_t)(3 * 64 * kWyLD + kWyCH * kWyLDY + 64) * sizeof(double);
+constexpr int kWyLD = 64 + 4;  // 64 x 64 smem matrices and Y chunks: element (r, c) at [c * LD + r]
+constexpr int kWyCH = 64;      // Y rows per staged chunk
+constexpr size_t kWySmem = (size_t)(5 * 64 * kWyLD + 64) * sizeof(double);
 
 BF_DEV void wy_dmma(double (&d)[2], double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(d[0]), "+d"(d[1])
                : "d"(a), "d"(b));
 }
-
-// Y[r][c] of the factored pair: 1 on the diagonal, the stored reflector below, 0 above
-BF_DEV double wy_y(const double* Pg, int m, int r, int c) {
-  return r > c ? Pg[(size_t)c * m + r] : (r == c ? 1.0 : 0.0);
+BF_DEV void wy_cp16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+BF_DEV void wy_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+BF_DEV void wy_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
 __global__ void __launch_bounds__(256) bj_dapply_wy(BJArgs<double> a, BDArgs d, int step) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int KK = 64, LD = kWyLD, LDY = kWyLDY, CH = kWyCH;
+  constexpr int KK = 64, LD = kWyLD, CH = kWyCH;
   const int P = a.nb / 2;
   const int64_t b = blockIdx.x / P;
   const int pk = blockIdx.x % P;
@@ -515,12 +518,35 @@ __global__ void __launch_bounds__(256) bj_dapply_wy(BJArgs<double> a, BDArgs d, 
   double* bufA = reinterpret_cast<double*>(smem_raw);
   double* bufB = bufA + 64 * LD;
   double* bufC = bufB + 64 * LD;
-  double* Ys = bufC + 64 * LD;  // CH x LDY
-  double* taus = Ys + CH * LDY;
+  double* Yb[2] = {bufC + 64 * LD, bufC + 2 * 64 * LD};  // double-buffered raw Y chunks
+  double* taus = bufC + 3 * 64 * LD;
   const double* Pg = d.P + slot * (int64_t)m * KK;
   const double* U = d.U + slot * KK * KK;
   const double* S = d.S + slot * KK;
   if (tid < KK) taus[tid] = d.tau[slot * KK + tid];
+  const int nch = (m + CH - 1) / CH;
+  // raw rows rc..rc+63 of the factored pair, column-major, 16-byte cp.async (rows >= m zero)
+  auto load = [&](int buf, int rc) {
+    double* Y = Yb[buf];
+    for (int e = tid; e < KK * (CH / 2); e += 256) {
+      const int c = e / (CH / 2), rr = 2 * (e % (CH / 2)), r = rc + rr;
+      double* dst = &Y[c * LD + rr];
+      const double* src = Pg + (size_t)c * m + r;
+      if (r + 1 < m && ((m & 1) == 0)) {
+        wy_cp16(dst, src);
+      } else {
+        dst[0] = r < m ? src[0] : 0.0;
+        dst[1] = r + 1 < m ? src[1] : 0.0;
+      }
+    }
+    wy_commit();
+  };
+  // Y[r][c] (unit lower trapezoidal): the stored reflector below the diagonal, 1 on it, 0 above;
+  // only the first chunk has rows <= c
+  auto yv = [&](const double* Y, int rl, int c, int rg) {
+    const double raw = Y[c * LD + rl];
+    return rg > c ? raw : (rg == c ? 1.0 : 0.0);
+  };
   double acc[2][4][2];
   auto zero = [&]() {
 #pragma unroll
@@ -536,29 +562,39 @@ __global__ void __launch_bounds__(256) bj_dapply_wy(BJArgs<double> a, BDArgs d, 
 #pragma unroll
         for (int q = 0; q < 2; ++q) M[(c0 + 8 * y + 2 * t + q) * LD + r0 + 8 * x + g] = acc[x][y][q];
   };
-  // ---- G_Y = Y^T Y (accumulated over row chunks of Y)
+  // ---- G_Y = Y^T Y, accumulated over double-buffered row chunks of Y
   zero();
-  for (int rc = 0; rc < m; rc += CH) {
-    __syncthreads();
-    for (int e = tid; e < CH * KK; e += 256) {  // column-major walk: coalesced reads of Pg
-      const int c = e / CH, rr = e % CH, r = rc + rr;
-      Ys[rr * LDY + c] = r < m ? wy_y(Pg, m, r, c) : 0.0;
+  load(0, 0);
+  for (int ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) {
+      load((ch + 1) & 1, (ch + 1) * CH);
+      wy_wait<1>();
+    } else {
+      wy_wait<0>();
     }
     __syncthreads();
-#pragma unroll
+    const double* Y = Yb[ch & 1];
+    const int rc = ch * CH;
+#pragma unroll 4
     for (int k0 = 0; k0 < CH; k0 += 4) {
       double av[2], bv[4];
+      const int rl = k0 + t, rg = rc + rl;
 #pragma unroll
-      for (int x = 0; x < 2; ++x) av[x] = Ys[(k0 + t) * LDY + r0 + 8 * x + g];  // A[i][k] = Y[k][i]
+      for (int x = 0; x < 2; ++x) av[x] = yv(Y, rl, r0 + 8 * x + g, rg);  // A[i][k] = Y[k][i]
 #pragma unroll
-      for (int y = 0; y < 4; ++y) bv[y] = Ys[(k0 + t) * LDY + c0 + 8 * y + g];  // B[k][j] = Y[k][j]
+      for (int y = 0; y < 4; ++y) bv[y] = yv(Y, rl, c0 + 8 * y + g, rg);  // B[k][j] = Y[k][j]
 #pragma unroll
       for (int x = 0; x < 2; ++x)
 #pragma unroll
         for (int y = 0; y < 4; ++y) wy_dmma(acc[x][y], av[x], bv[y]);
     }
+    __syncthreads();
   }
   store(bufA);  // G_Y
+  // chunk 0 (Y1, and the first chunk of the final product) into the buffer not holding the
+  // last chunk; it streams in while T is formed
+  const int z = nch & 1;
+  load(z, 0);
   // ---- X1 = U_R diag(sigma) -> bufC
   for (int e = tid; e < KK * KK; e += 256) {
     const int c = e / KK, r = e % KK;
@@ -571,9 +607,9 @@ __global__ void __launch_bounds__(256) bj_dapply_wy(BJArgs<double> a, BDArgs d, 
       const int i = tid;
       double v = 0.0;
       if (i < j) {
-        double z = 0.0;
-        for (int l = i; l < j; ++l) z = fma(bufB[l * LD + i], bufA[j * LD + l], z);
-        v = -taus[j] * z;
+        double zz = 0.0;
+        for (int l = i; l < j; ++l) zz = fma(bufB[l * LD + i], bufA[j * LD + l], zz);
+        v = -taus[j] * zz;
       } else if (i == j) {
         v = taus[j];
       }
@@ -581,29 +617,28 @@ __global__ void __launch_bounds__(256) bj_dapply_wy(BJArgs<double> a, BDArgs d, 
     }
     __syncthreads();
   }
+  wy_wait<0>();
+  __syncthreads();
   // ---- W1 = Y1^T X1 (Y1 = top 64 rows of Y) -> bufA
   zero();
-  for (int rc = 0; rc < KK; rc += CH) {
-    for (int e = tid; e < CH * KK; e += 256) {
-      const int c = e / CH, rr = e % CH, r = rc + rr;
-      Ys[rr * LDY + c] = wy_y(Pg, m, r, c);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k0 = 0; k0 < CH; k0 += 4) {
+  {
+    const double* Y = Yb[z];
+#pragma unroll 4
+    for (int k0 = 0; k0 < KK; k0 += 4) {
       double av[2], bv[4];
 #pragma unroll
-      for (int x = 0; x < 2; ++x) av[x] = Ys[(k0 + t) * LDY + r0 + 8 * x + g];               // Y1[k][i]
+      for (int x = 0; x < 2; ++x) av[x] = yv(Y, k0 + t, r0 + 8 * x + g, k0 + t);  // Y1[k][i]
 #pragma unroll
-      for (int y = 0; y < 4; ++y) bv[y] = bufC[(c0 + 8 * y + g) * LD + rc + k0 + t];       // X1[k][j]
+      for (int y = 0; y < 4; ++y) bv[y] = bufC[(c0 + 8 * y + g) * LD + k0 + t];  // X1[k][j]
 #pragma unroll
       for (int x = 0; x < 2; ++x)
 #pragma unroll
         for (int y = 0; y < 4; ++y) wy_dmma(acc[x][y], av[x], bv[y]);
     }
-    __syncthreads();
   }
+  __syncthreads();
   store(bufA);  // W1 (G_Y no longer needed)
+  if (nch > 1) load(z ^ 1, CH);  // the final product's second chunk
   __syncthreads();
   // ---- W2 = T W1 -> bufC (X1 is re-read from U, S below)
   zero();
@@ -621,34 +656,35 @@ __global__ void __launch_bounds__(256) bj_dapply_wy(BJArgs<double> a, BDArgs d, 
   }
   __syncthreads();
   store(bufC);
-  // ---- new pair = [X1; 0] - Y W2, 64-row chunks of Y, written straight to W
+  // ---- new pair = [X1; 0] - Y W2, 64-row chunks of Y (double-buffered), written to W
   double* Wb = a.W + b * (int64_t)m * a.n_pad;
-  for (int rc = 0; rc < m; rc += 64) {
-    zero();
-    for (int half = 0; half < 64; half += CH) {
-      __syncthreads();
-      for (int e = tid; e < CH * KK; e += 256) {
-        const int c = e / CH, rr = e % CH, r = rc + half + rr;
-        Ys[rr * LDY + c] = r < m ? wy_y(Pg, m, r, c) : 0.0;
-      }
-      __syncthreads();
-      // rows r0..r0+15 of this 64-row chunk live in the half that contains them
-      if ((r0 >= half) && (r0 < half + CH)) {
-        const int rl = r0 - half;
-#pragma unroll 4
-        for (int k0 = 0; k0 < KK; k0 += 4) {
-          double av[2], bv[4];
-#pragma unroll
-          for (int x = 0; x < 2; ++x) av[x] = Ys[(rl + 8 * x + g) * LDY + k0 + t];  // Y[i][k]
-#pragma unroll
-          for (int y = 0; y < 4; ++y) bv[y] = bufC[(c0 + 8 * y + g) * LD + k0 + t];  // W2[k][j]
-#pragma unroll
-          for (int x = 0; x < 2; ++x)
-#pragma unroll
-            for (int y = 0; y < 4; ++y) wy_dmma(acc[x][y], av[x], bv[y]);
-        }
-      }
+  for (int ch = 0; ch < nch; ++ch) {
+    const int buf = (z + ch) & 1, rc = ch * CH;
+    if (ch + 1 < nch) {
+      wy_wait<1>();
+    } else {
+      wy_wait<0>();
     }
+    __syncthreads();
+    const double* Y = Yb[buf];
+    zero();
+#pragma unroll 4
+    for (int k0 = 0; k0 < KK; k0 += 4) {
+      double av[2], bv[4];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const int rl = r0 + 8 * x + g;
+        av[x] = yv(Y, rl, k0 + t, rc + rl);  // Y[i][k]
+      }
+#pragma unroll
+      for (int y = 0; y < 4; ++y) bv[y] = bufC[(c0 + 8 * y + g) * LD + k0 + t];  // W2[k][j]
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) wy_dmma(acc[x][y], av[x], bv[y]);
+    }
+    __syncthreads();  // buffer `buf` is free
+    if (ch + 2 < nch) load(buf, (ch + 2) * CH);
 #pragma unroll
     for (int x = 0; x < 2; ++x) {
       const int r = rc + r0 + 8 * x + g;
