@@ -580,8 +580,9 @@ class SvdChoice:
     seed: int = 0
 
 
-def _factor(A, choice, level):
-    """Batched SVD of (B, M, N), M >= N: returns u (B, M, w), s (B, w) descending, v (B, N, w).
+def _factor(A, choice, level, need_v=True):
+    """Batched SVD of (B, M, N), M >= N: returns u (B, M, w), s (B, w) descending, v (B, N, w)
+    (v is None for ``full`` when not ``need_v``: the Jacobi sweeps then skip V entirely).
 
     ``full``: the one-sided Jacobi tiers (bf_svd_batched: register tier up to 64 columns, else
     the shared-memory tier); ``block``: block Jacobi, direct method (bf_block_svd_batched, the
@@ -612,9 +613,9 @@ def _factor(A, choice, level):
         from .qr import qr_tensor
 
         q, rr = qr_tensor(A)
-        r = svd_tensor(rr.contiguous(), JacobiOptions(ordering="round_robin", accumulate_v=True))
+        r = svd_tensor(rr.contiguous(), JacobiOptions(ordering="round_robin", accumulate_v=need_v))
         return bmm(q.contiguous(), r["u"].contiguous()), r["sigma"], r["v"]
-    r = svd_tensor(A, JacobiOptions(ordering="round_robin", accumulate_v=True))
+    r = svd_tensor(A, JacobiOptions(ordering="round_robin", accumulate_v=need_v))
     return r["u"], r["sigma"], r["v"]
 
 
@@ -636,7 +637,13 @@ def _node_svd(A, nz, k, choice, level):
     parts = []
     if len(tall):
         idx = torch.as_tensor(tall, device=dev)
-        u, s, v = _factor(A[idx], choice, level)
+        At = A[idx]
+        u, s, v = _factor(At, choice, level, need_v=False)
+        if v is None:
+            # T = diag(sigma) W^T = U^T A: the right vectors are never needed on their own, so the
+            # sweeps skip V and W diag(sigma) = A^T U comes from one batched GEMM
+            vs = bmm(At, u.contiguous(), ta=True)  # (b, k, w)
+            v = vs / torch.where(s > 0, s, torch.ones_like(s))[:, None, :]
         parts.append((idx, u, s, v))
     if len(wide):
         idx = torch.as_tensor(wide, device=dev)
