@@ -114,10 +114,14 @@ BF_DEV void jacobi_rotation(double gpp, double gpq, double gqq, double& c, doubl
 // (jacobi.py:102-115): idx_t[0] = 0, idx_t[j] = 1 + ((j - 1 - t) mod (nw - 1)),
 // pair k = (idx_t[k], idx_t[nw-1-k]) normalised so p < q.
 BF_DEV void rr_pair(int nw, int st, int k, int& p, int& q) {
-  int L = nw - 1;
-  int a = (k == 0) ? 0 : 1 + (((k - 1 - st) % L) + L) % L;
-  int j = nw - 1 - k;
-  int b = 1 + (((j - 1 - st) % L) + L) % L;
+  // circle method positions without integer division: 0 <= st < L, so both offsets lie in [-L, L)
+  const int L = nw - 1;
+  int x = k - 1 - st;
+  x += x < 0 ? L : 0;
+  const int a = (k == 0) ? 0 : 1 + x;
+  int y = (nw - 1 - k) - 1 - st;
+  y += y < 0 ? L : 0;
+  const int b = 1 + y;
   p = a < b ? a : b;
   q = a < b ? b : a;
 }

@@ -59,15 +59,24 @@ BF_DEV long long jacobi_step(T* W, int ldw, T* V, int ldv, int m, int nw, int or
         gqq[j] += shfl_xor(gqq[j], o);
       }
     }
+    // the PB rotations are independent: form them all before applying any (their latency
+    // chains overlap instead of serialising with the column updates)
+    T cj[PB], sj[PB];
+    bool doit[PB];
 #pragma unroll
     for (int j = 0; j < PB; ++j) {
-      if (pp[j] < 0) continue;
       double dpp = (double)gpp[j], dpq = (double)gpq[j], dqq = (double)gqq[j];
       // skip rule (jacobi.py:134 / :167): |g_pq|^2 <= tol^2 g_pp g_qq
-      if (!(dpq * dpq > tol2 * (dpp * dqq))) continue;
-      double cd, sd;
-      jacobi_rotation(dpp, dpq, dqq, cd, sd);
-      const T c = (T)cd, s = (T)sd;
+      doit[j] = pp[j] >= 0 && dpq * dpq > tol2 * (dpp * dqq);
+      double cd = 1.0, sd = 0.0;
+      if (doit[j]) jacobi_rotation(dpp, dpq, dqq, cd, sd);
+      cj[j] = (T)cd;
+      sj[j] = (T)sd;
+    }
+#pragma unroll
+    for (int j = 0; j < PB; ++j) {
+      if (!doit[j]) continue;
+      const T c = cj[j], s = sj[j];
       ++rot;
       T* wp = W + (size_t)pp[j] * ldw;
       T* wq = W + (size_t)qq[j] * ldw;

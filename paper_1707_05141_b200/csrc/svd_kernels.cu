@@ -47,29 +47,32 @@ static size_t svd_smem_bytes(int m, int nw, bool accv, bool in_smem) {
   return (b + 15) & ~(size_t)15;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(512) svd_cta_kernel(SvdArgs<T> a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int64_t b = blockIdx.x;
-  if (b >= a.batch) return;
-  if (a.active && !a.active[b]) return;
+// MODE 0: W, V, candidates in shared memory; 1: W + candidates in shared memory, V in global;
+// 2: everything in the global workspace. Separate instantiations so the shared-memory operands
+// are addressed as such (LDS/STS, not generic loads).
+template <typename T, int MODE>
+BF_DEV void svd_cta_body(const SvdArgs<T>& a, unsigned char* smem_raw, int64_t b) {
   const int m = a.m, n = a.n, nw = a.nw;
   const bool accv = a.v != nullptr;
   T* W;
   T* V;
   T* cand;
   size_t smem_elems;
-  if (a.in_smem || !a.w_in_smem) {  // W, V, candidates contiguous, all in smem or all in global
-    T* base = a.in_smem ? reinterpret_cast<T*>(smem_raw) : a.gws + b * a.gws_stride;
-    W = base;
+  if (MODE == 0) {
+    W = reinterpret_cast<T*>(smem_raw);
     V = accv ? W + (size_t)m * nw : nullptr;
     cand = W + (size_t)m * nw + (accv ? (size_t)nw * nw : 0);
-    smem_elems = a.in_smem ? svd_work_elems<T>(m, nw, accv) : 0;
-  } else {  // W + candidates in smem, V (touched once per rotation) in global / L2
+    smem_elems = svd_work_elems<T>(m, nw, accv);
+  } else if (MODE == 1) {
     W = reinterpret_cast<T*>(smem_raw);
     cand = W + (size_t)m * nw;
     V = accv ? a.gws + b * a.gws_stride : nullptr;
     smem_elems = svd_work_elems<T>(m, nw, false);
+  } else {
+    W = a.gws + b * a.gws_stride;
+    V = accv ? W + (size_t)m * nw : nullptr;
+    cand = W + (size_t)m * nw + (accv ? (size_t)nw * nw : 0);
+    smem_elems = 0;
   }
   unsigned char* tail = smem_raw + smem_elems * sizeof(T);
   T* sig = reinterpret_cast<T*>(tail);
@@ -90,7 +93,6 @@ __global__ void __launch_bounds__(512) svd_cta_kernel(SvdArgs<T> a) {
   if (accv)
     for (int64_t e = tid; e < (int64_t)nw * nw; e += blockDim.x) V[e] = (e / nw == e % nw) ? T(1) : T(0);
   __syncthreads();
-
   SweepStats st = jacobi_sweeps<T, 4>(W, m, V, nw, m, n, nw, a.ordering, a.tol, a.max_sweeps, counters);
   if (!st.converged) {
     double off = off_orthogonality_cta<T>(W, m, m, nw, sig, red);
@@ -106,6 +108,20 @@ __global__ void __launch_bounds__(512) svd_cta_kernel(SvdArgs<T> a) {
 }
 
 static int working_cols(int n, int ordering) { return (ordering == 1 && (n & 1)) ? n + 1 : n; }
+
+template <typename T>
+__global__ void __launch_bounds__(512) svd_cta_kernel(SvdArgs<T> a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int64_t b = blockIdx.x;
+  if (b >= a.batch) return;
+  if (a.active && !a.active[b]) return;
+  if (a.in_smem)
+    svd_cta_body<T, 0>(a, smem_raw, b);
+  else if (a.w_in_smem)
+    svd_cta_body<T, 1>(a, smem_raw, b);
+  else
+    svd_cta_body<T, 2>(a, smem_raw, b);
+}
 
 static bool fits_smem(size_t bytes) { return bytes <= 227 * 1024; }
 
