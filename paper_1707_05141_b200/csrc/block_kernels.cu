@@ -518,7 +518,7 @@ __global__ void __launch_bounds__(256) bj_dapply_wy(BJArgs<double> a, BDArgs d, 
   double* bufA = reinterpret_cast<double*>(smem_raw);
   double* bufB = bufA + 64 * LD;
   double* bufC = bufB + 64 * LD;
-  double* Yb[2] = {bufC + 64 * LD, bufC + 2 * 64 * LD};  // double-buffered raw Y chunks
+  double* const Ybase = bufC + 64 * LD;  // double-buffered raw Y chunks at Ybase + buf * 64 * LD
   double* taus = bufC + 3 * 64 * LD;
   const double* Pg = d.P + slot * (int64_t)m * KK;
   const double* U = d.U + slot * KK * KK;
@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(256) bj_dapply_wy(BJArgs<double> a, BDArgs d, 
   const int nch = (m + CH - 1) / CH;
   // raw rows rc..rc+63 of the factored pair, column-major, 16-byte cp.async (rows >= m zero)
   auto load = [&](int buf, int rc) {
-    double* Y = Yb[buf];
+    double* Y = Ybase + buf * (64 * LD);
     for (int e = tid; e < KK * (CH / 2); e += 256) {
       const int c = e / (CH / 2), rr = 2 * (e % (CH / 2)), r = rc + rr;
       double* dst = &Y[c * LD + rr];
@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(256) bj_dapply_wy(BJArgs<double> a, BDArgs d, 
       wy_wait<0>();
     }
     __syncthreads();
-    const double* Y = Yb[ch & 1];
+    const double* Y = Ybase + (ch & 1) * (64 * LD);
     const int rc = ch * CH;
 #pragma unroll 4
     for (int k0 = 0; k0 < CH; k0 += 4) {
@@ -601,28 +601,26 @@ __global__ void __launch_bounds__(256) bj_dapply_wy(BJArgs<double> a, BDArgs d, 
     bufC[c * LD + r] = U[(size_t)c * KK + r] * S[c];
   }
   __syncthreads();
-  // ---- T (upper triangular) -> bufB, column by column
-  for (int j = 0; j < KK; ++j) {
-    if (tid < KK) {
-      const int i = tid;
-      double v = 0.0;
-      if (i < j) {
-        double zz = 0.0;
-        for (int l = i; l < j; ++l) zz = fma(bufB[l * LD + i], bufA[j * LD + l], zz);
-        v = -taus[j] * zz;
-      } else if (i == j) {
-        v = taus[j];
-      }
-      bufB[j * LD + i] = v;
+  // ---- T (upper triangular) -> bufB, column by column; the dot of row i is split over the 4
+  // threads (i, q) (l = i + q mod 4) and summed by two shuffles, so all 256 threads work
+  {
+    const int i = tid >> 2, q = tid & 3;
+    for (int j = 0; j < KK; ++j) {
+      double zz = 0.0;
+      if (i < j)
+        for (int l = i + q; l < j; l += 4) zz = fma(bufB[l * LD + i], bufA[j * LD + l], zz);
+      zz += __shfl_xor_sync(0xffffffffu, zz, 1);
+      zz += __shfl_xor_sync(0xffffffffu, zz, 2);
+      if (q == 0) bufB[j * LD + i] = i < j ? -taus[j] * zz : (i == j ? taus[j] : 0.0);
+      __syncthreads();
     }
-    __syncthreads();
   }
   wy_wait<0>();
   __syncthreads();
   // ---- W1 = Y1^T X1 (Y1 = top 64 rows of Y) -> bufA
   zero();
   {
-    const double* Y = Yb[z];
+    const double* Y = Ybase + z * (64 * LD);
 #pragma unroll 4
     for (int k0 = 0; k0 < KK; k0 += 4) {
       double av[2], bv[4];
@@ -666,7 +664,7 @@ __global__ void __launch_bounds__(256) bj_dapply_wy(BJArgs<double> a, BDArgs d, 
       wy_wait<0>();
     }
     __syncthreads();
-    const double* Y = Yb[buf];
+    const double* Y = Ybase + buf * (64 * LD);
     zero();
 #pragma unroll 4
     for (int k0 = 0; k0 < KK; k0 += 4) {
