@@ -278,3 +278,14 @@ def test_compress_cli(tmp_path):
     rec = json.loads(out.read_text().splitlines()[-1])
     assert rec["ranks_after"][-1] <= 64 and rec["error_estimate"] <= 1e-7
     assert rec["memory_after"]["dense"] == rec["memory_before"]["dense"]
+
+
+@pytest.mark.gpu
+def test_projection_tree_norm_on_orthonormal_basis():
+    """||T||_2 <= 1 + 1e-12 when T projects an orthonormal basis (a compressed H)."""
+    H = h2.build_h2(h2.perturbed_grid(2500, seed=1), 0.1, 11, 2.0, 64)
+    Hc, _ = h2.compress(_cuda(H), 1e-7)
+    _, _, _, T, _ = h2.truncate_basis(Hc, 1e-7)
+    for t in T:
+        if t is not None and t.numel():
+            assert float(torch.linalg.matrix_norm(t.double().cpu(), ord=2).max()) <= 1 + 1e-12
