@@ -68,8 +68,8 @@ BF_DEV long long jacobi_step(T* W, int ldw, T* V, int ldv, int m, int nw, int or
       double dpp = (double)gpp[j], dpq = (double)gpq[j], dqq = (double)gqq[j];
       // skip rule (jacobi.py:134 / :167): |g_pq|^2 <= tol^2 g_pp g_qq
       doit[j] = pp[j] >= 0 && dpq * dpq > tol2 * (dpp * dqq);
-      double cd = 1.0, sd = 0.0;
-      if (doit[j]) jacobi_rotation(dpp, dpq, dqq, cd, sd);
+      double cd = 1.0, sd = 0.0, td;
+      if (doit[j]) jacobi_rotation_t(dpp, dpq, dqq, cd, sd, td);
       cj[j] = (T)cd;
       sj[j] = (T)sd;
     }

@@ -59,39 +59,6 @@ struct RegCfg {
 // Named barrier among the WW row-warps of the CTA (id 1).
 BF_DEV void named_bar(int id, int nthreads) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory"); }
 
-// Rutishauser rotation returning t as well (jacobi.py:68-80), g_pq != 0:
-//   zeta = (g_qq - g_pp) / (2 g_pq), t = sign(zeta) / (|zeta| + hypot(1, zeta)),
-//   c = 1 / hypot(1, t), s = c t.
-// Evaluated without forming zeta: with den = 2 g_pq, diff = g_qq - g_pp and
-// h = hypot(diff, den), dd = |diff| + h:  t = sign(zeta) |den| / dd,
-// c = dd / hypot(dd, den), s = sign(zeta) |den| / hypot(dd, den) -- the same quantities
-// multiplied through by |den|, which leaves two independent reciprocal chains (t and c, s)
-// after h instead of four dependent ones. Exact IEEE fallback outside [1e-150, 1e150].
-BF_DEV void jacobi_rotation_t(double gpp, double gpq, double gqq, double& c, double& s, double& t) {
-  const double den = 2.0 * gpq, diff = gqq - gpp;
-  const double aden = fabs(den), adiff = fabs(diff);
-  const double big = aden > adiff ? aden : adiff;
-  if (big > 1e-150 && big < 1e150) {
-    // sign(zeta): zeta = diff / den carries the xor of both sign bits (signed zeros included)
-    const unsigned long long sb =
-        (unsigned long long)(__double_as_longlong(diff) ^ __double_as_longlong(den)) & 0x8000000000000000ULL;
-    const double sden = __longlong_as_double(__double_as_longlong(aden) | (long long)sb);
-    const double q = fma(diff, diff, den * den);
-    const double h = q * rsqrt_fast(q);  // hypot(diff, den)
-    const double dd = adiff + h;
-    const double q2 = fma(dd, dd, den * den);
-    const double r2 = rsqrt_fast(q2);  // 1 / hypot(dd, den)
-    t = sden * rcp_fast(dd);
-    c = dd * r2;
-    s = sden * r2;
-  } else {
-    const double zeta = diff / den;
-    t = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
-    c = 1.0 / hypot(1.0, t);
-    s = c * t;
-  }
-}
-
 // Step kinds: 0 round robin, 1 serial odd step, 2 serial even step.
 template <class C, int ORD>
 struct RegGeom {
