@@ -289,3 +289,14 @@ def test_projection_tree_norm_on_orthonormal_basis():
     for t in T:
         if t is not None and t.numel():
             assert float(torch.linalg.matrix_norm(t.double().cpu(), ord=2).max()) <= 1 + 1e-12
+
+
+def test_degenerate_points_build_and_matvec():
+    """All points identical (SPEC.md:554 ledger): the tree halves by index, nothing is
+    admissible, the operator is the exact dense kernel (all ones)."""
+    pts = np.full((300, 2), 0.25)
+    H = h2.build_h2(pts, 0.1, 4, 1.0, 64)
+    assert not H.coupling and all(H.tree.hi[i] - H.tree.lo[i] <= 64 for i in H.tree.leaves())
+    x = np.random.default_rng(2).standard_normal(300)
+    y = h2.h2_matvec(H.to(), torch.as_tensor(x)).numpy()
+    np.testing.assert_allclose(y, np.full(300, x.sum()), rtol=1e-12, atol=1e-12)
