@@ -305,81 +305,102 @@ __global__ void gaussian_kernel(int64_t batch, int rows, int cols, uint64_t seed
   int64_t k = 0;
   uint64_t pos = 0;
   while (k < total) {
+    // one batch: lane l holds stream words 4 (blk + l) .. 4 (blk + l) + 3
     const uint64_t blk = pos >> 2;
-    const int off = lane == 0 ? (int)(pos & 3) : 0;  // words of lane 0 before pos are consumed
+    const uint64_t bend = (blk + 32) * 4;
     uint64_t w[4];
     philox_block(k0, k1, blk + lane, w);
     double x[4];
-    int rej = 4;  // first (valid) word of this lane failing the fast path
+    bool fast[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const uint64_t r = w[q];
       const int idx = (int)(r & 0xff);
       const uint64_t rr = r >> 8;
       const uint64_t rabs = (rr >> 1) & 0x000fffffffffffffULL;
-      double v = (double)rabs * bf_zig_wi[idx];
+      const double v = (double)rabs * bf_zig_wi[idx];
       x[q] = (rr & 1) ? -v : v;
-      if (q >= off && rej == 4 && !(rabs < bf_zig_ki[idx])) rej = q;
+      fast[q] = rabs < bf_zig_ki[idx];
     }
-    const unsigned bal = __ballot_sync(FULL, rej < 4);
-    const int L = bal ? __ffs(bal) - 1 : 32;
-    const int cnt = lane < L ? 4 - off : (lane == L ? rej - off : 0);
-    int incl = cnt;
+    // the batch is consumed from `pos` on; every slow-path event is resolved inside it (its
+    // extra words come from the batch's registers when they lie in it), so Philox runs once
+    // per 128 words instead of once per event
+    while (k < total && pos < bend) {
+      const uint64_t lane0 = (blk + lane) * 4;  // stream position of this lane's word 0
+      int rej = 4;
+      int first = 4;  // first unconsumed word of this lane
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int y = __shfl_up_sync(FULL, incl, d);
-      if (lane >= d) incl += y;
-    }
-    const int start = incl - cnt;
-    const int tot = __shfl_sync(FULL, incl, 31);
+      for (int q = 0; q < 4; ++q) {
+        const bool live = lane0 + q >= pos;
+        first = (live && first == 4) ? q : first;
+        if (live && rej == 4 && !fast[q]) rej = q;
+      }
+      const unsigned bal = __ballot_sync(FULL, rej < 4);
+      const int L = bal ? __ffs(bal) - 1 : 32;
+      const int cnt = lane < L ? 4 - first : (lane == L ? rej - first : 0);
+      int incl = cnt;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (q >= off && q - off < cnt) store(k + start + (q - off), x[q]);
-    k += tot;
-    if (L == 32) {
-      pos = (blk + 32) * 4;
-      continue;
-    }
-    // slow path for the candidate word (L, rej_L)
-    const int q_s = __shfl_sync(FULL, rej, L);
-    uint64_t r_s = w[0];
+      for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, d);
+        if (lane >= d) incl += y;
+      }
+      const int start = incl - cnt;
+      const int tot = __shfl_sync(FULL, incl, 31);
 #pragma unroll
-    for (int q = 1; q < 4; ++q) r_s = q == q_s ? w[q] : r_s;
-    r_s = __shfl_sync(FULL, r_s, L);
-    uint64_t p = (blk + L) * 4 + q_s + 1;
-    int produced = 0;
-    if (lane == 0 && k < total) {
-      const int idx_s = (int)(r_s & 0xff);
-      const uint64_t rr = r_s >> 8;
-      const uint64_t rabs_s = (rr >> 1) & 0x000fffffffffffffULL;
-      double xs = (double)rabs_s * bf_zig_wi[idx_s];
-      if (rr & 1) xs = -xs;
-      double val = 0.0;
-      if (idx_s == 0) {
-        for (;;) {
-          double xx = -BF_ZIG_NOR_INV_R * log1p(-u01(philox_word(k0, k1, p)));
-          double yy = -log1p(-u01(philox_word(k0, k1, p + 1)));
-          p += 2;
-          if (yy + yy > xx * xx) {
-            val = ((rabs_s >> 8) & 0x1) ? -(BF_ZIG_NOR_R + xx) : BF_ZIG_NOR_R + xx;
+      for (int q = 0; q < 4; ++q)
+        if (q >= first && q - first < cnt) store(k + start + (q - first), x[q]);
+      k += tot;
+      if (L == 32) {
+        pos = bend;
+        break;
+      }
+      // slow path for the first failing word (lane L, word q_s) at stream position ps
+      const int q_s = __shfl_sync(FULL, rej, L);
+      uint64_t r_s = w[0];
+#pragma unroll
+      for (int q = 1; q < 4; ++q) r_s = q == q_s ? w[q] : r_s;
+      r_s = __shfl_sync(FULL, r_s, L);
+      uint64_t p = (blk + L) * 4 + q_s + 1;
+      // the wedge test's uniform is the next word: from the batch when it is in it
+      const int lw = (int)((p >> 2) - blk), qw = (int)(p & 3);
+      uint64_t r_u = w[0];
+#pragma unroll
+      for (int q = 1; q < 4; ++q) r_u = q == qw ? w[q] : r_u;
+      r_u = __shfl_sync(FULL, r_u, lw < 32 ? lw : 0);
+      int produced = 0;
+      if (lane == 0 && k < total) {
+        const int idx_s = (int)(r_s & 0xff);
+        const uint64_t rr = r_s >> 8;
+        const uint64_t rabs_s = (rr >> 1) & 0x000fffffffffffffULL;
+        double xs = (double)rabs_s * bf_zig_wi[idx_s];
+        if (rr & 1) xs = -xs;
+        double val = 0.0;
+        if (idx_s == 0) {
+          for (;;) {
+            double xx = -BF_ZIG_NOR_INV_R * log1p(-u01(philox_word(k0, k1, p)));
+            double yy = -log1p(-u01(philox_word(k0, k1, p + 1)));
+            p += 2;
+            if (yy + yy > xx * xx) {
+              val = ((rabs_s >> 8) & 0x1) ? -(BF_ZIG_NOR_R + xx) : BF_ZIG_NOR_R + xx;
+              produced = 1;
+              break;
+            }
+          }
+        } else {
+          const double u = u01(lw < 32 ? r_u : philox_word(k0, k1, p));
+          p += 1;
+          if (((bf_zig_fi[idx_s - 1] - bf_zig_fi[idx_s]) * u + bf_zig_fi[idx_s]) < exp(-0.5 * xs * xs)) {
+            val = xs;
             produced = 1;
-            break;
           }
         }
-      } else {
-        double u = u01(philox_word(k0, k1, p));
-        p += 1;
-        if (((bf_zig_fi[idx_s - 1] - bf_zig_fi[idx_s]) * u + bf_zig_fi[idx_s]) < exp(-0.5 * xs * xs)) {
-          val = xs;
-          produced = 1;
-        }
+        if (produced) store(k, val);
       }
-      if (produced) store(k, val);
+      produced = __shfl_sync(FULL, produced, 0);
+      p = __shfl_sync(FULL, p, 0);
+      k += produced;
+      pos = p;
     }
-    produced = __shfl_sync(FULL, produced, 0);
-    p = __shfl_sync(FULL, p, 0);
-    k += produced;
-    pos = p;
   }
 }
 
