@@ -19,11 +19,15 @@ namespace bf {
 namespace {
 
 
+// barrier of the WW warps holding one matrix; with several matrices per CTA (kernel template
+// G) each group of WW warps uses its own named barrier 1 + group
 BF_DEV void wbar(int ww) {
-  if (ww > 1)
-    asm volatile("bar.sync 1, %0;" ::"r"(ww * 32) : "memory");
-  else
+  if (ww > 1) {
+    const int id = 1 + (int)(threadIdx.x >> 5) / ww;
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(ww * 32) : "memory");
+  } else {
     __syncwarp();
+  }
 }
 
 // Sum over all rows (all lanes of all WW warps) of K per-lane partials; result in p[] on every
@@ -208,24 +212,27 @@ struct QrReg {
   }
 };
 
-// G > 1 (single-warp configurations only): G independent warps per CTA, each on its own
-// matrix with its own shared-memory slice. The unrolled kernel is tens of thousands of
+// G > 1: G independent groups of WW warps per CTA, each on its own matrix with its own
+// shared-memory slice (and named barrier). The unrolled kernel is tens of thousands of
 // instructions long; warps launched together walk it roughly in step and share i-cache lines.
+#ifndef BF_QR40_G
+#define BF_QR40_G 1  // measured: G = 2 is slower for 128x40 (1.98 vs 1.93 ms)
+#endif
 #ifndef BF_QR_G
 #define BF_QR_G 4  // measured: 64x32 x10000 0.590 -> 0.571 ms (G = 2: 0.580)
 #endif
 template <int N, int R, int WW, int G = 1>
 __global__ void __launch_bounds__(WW * 32 * G) qr_reg_kernel(int64_t batch, int m, const double* A, int64_t as,
                                                              double* Q, int64_t qs, double* Rout, int64_t rs) {
-  static_assert(G == 1 || WW == 1, "grouped CTAs hold single-warp matrices");
+  static_assert(G * WW <= 15, "one named barrier per matrix group");
   __shared__ double tb_all[G][WW * 32 * QrReg<N, R, WW>::TSN];
   __shared__ double wsum_all[G][64];
   __shared__ double tau_all[G][N];
-  const int grp = G > 1 ? (int)(threadIdx.x >> 5) : 0;
+  const int grp = G > 1 ? (int)(threadIdx.x / (WW * 32)) : 0;
   double* tb = tb_all[grp];
   double* wsum = wsum_all[grp];
   double* tau_s = tau_all[grp];
-  const int tid = G > 1 ? (int)(threadIdx.x & 31) : (int)threadIdx.x;
+  const int tid = G > 1 ? (int)(threadIdx.x % (WW * 32)) : (int)threadIdx.x;
   for (int64_t b = (int64_t)blockIdx.x * G + grp; b < batch; b += (int64_t)gridDim.x * G) {
     const double* Ab = A + b * as;
     double a[R][N];
@@ -285,7 +292,7 @@ int launch_qr_reg(int dtype, int64_t batch, int m, int n, const void* a, int64_t
   double* Rr = (double*)r;
   if (n == 32 && m <= 64) return launch_qr_reg_t<32, 2, 1, BF_QR_G>(batch, m, A, as, Q, qs, Rr, rs, st);
   if (n == 16 && m <= 64) return launch_qr_reg_t<16, 2, 1>(batch, m, A, as, Q, qs, Rr, rs, st);
-  if (n == 40 && m <= 128) return launch_qr_reg_t<40, 2, 2>(batch, m, A, as, Q, qs, Rr, rs, st);
+  if (n == 40 && m <= 128) return launch_qr_reg_t<40, 2, 2, BF_QR40_G>(batch, m, A, as, Q, qs, Rr, rs, st);
   return -1;
 }
 
