@@ -309,6 +309,24 @@ def test_rsvd_golden(nm):
     assert vec_mismatch(r.v[:, :k], c["v"][:, :k], c["s"][:k], a.dtype, factor=4096.0) <= 1.0
 
 
+def test_rsvd_f32_with_caller_omega_vs_oracle():
+    """f32 rsvd (the caller supplies the sketch: numpy's float32 ziggurat is a different stream)
+    against the oracle on the same Omega; gate 1e-5 normwise (north star, f32)."""
+    B, m, n, k, p = 16, 128, 96, 24, 8
+    rng = np.random.default_rng(7)
+    a = rng.standard_normal((B, m, n)).astype(np.float32)
+    om = rng.standard_normal((B, n, k + p)).astype(np.float32)
+    r = bf.rsvd_tensor(torch.as_tensor(a).cuda(), bf.RsvdOptions(k=k, p=p, seed=3), omega=torch.as_tensor(om).cuda())
+    o = orc.batch_rsvd_stacked(np.ascontiguousarray(a.transpose(0, 2, 1)), m, n, k, p, seed=3,
+                               omega3=np.ascontiguousarray(om.transpose(0, 2, 1)), threads=8)
+    s = r["s"].cpu().numpy()
+    for b in range(B):
+        assert sigma_normwise(s[b], o["s"][b]) <= 1e-5
+    u = r["u"].cpu().double()
+    orth = (u.transpose(1, 2) @ u - torch.eye(k + p, dtype=torch.float64)).abs().max()
+    assert float(orth) < 1e-4
+
+
 def test_rsvd_cfg5_batch_vs_oracle():
     B = 64
     a, sig = bf.make_matrix_tensor(B, 128, 128, 1e16, rank=64, seed=5_000_000)
