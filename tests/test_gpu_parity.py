@@ -180,6 +180,24 @@ def test_svd_shared_tier_v_in_global(shape):
         assert vec_mismatch(v[b].T, o["v"][b].T, o["s"][b], np.float64) <= 1.0
 
 
+@pytest.mark.parametrize("ordering", ["serial", "round_robin"])
+def test_svd_f32_shared_tier_vs_oracle(ordering):
+    """f32 through the shared-memory tier (96 x 80: beyond the register tier) vs the oracle."""
+    B, m, n = 8, 96, 80
+    a = np.random.default_rng(11).standard_normal((B, m, n)).astype(np.float32)
+    r = bf.svd_tensor(torch.as_tensor(a).cuda(), bf.JacobiOptions(ordering=ordering, accumulate_v=True))
+    o = orc.batch_svd_stacked(np.ascontiguousarray(a.transpose(0, 2, 1)), m, n, ordering=ordering,
+                              accumulate_v=True, threads=8)
+    s = r["sigma"].cpu().numpy()
+    sw = r["sweeps"].cpu().numpy()
+    for b in range(B):
+        assert sigma_normwise(s[b], o["s"][b]) <= 1e-5
+        assert abs(int(sw[b]) - int(o["sweeps"][b])) <= 1
+    ad = torch.as_tensor(a, dtype=torch.float64)
+    rec = (r["u"].cpu().double() * r["sigma"].cpu().double()[:, None, :]) @ r["v"].cpu().double().transpose(1, 2)
+    assert float(((ad - rec).norm(dim=(1, 2)) / ad.norm(dim=(1, 2))).max()) < 1e-5
+
+
 def test_svd_cfg1_full_batch_properties():
     a = dev_gauss(1000, 32, 32, 1_000_000)
     r = bf.svd_tensor(a, bf.JacobiOptions(ordering="serial", accumulate_v=True))
