@@ -79,7 +79,7 @@ int svd_impl(int64_t batch, int m, int n, const T* a, T* u, T* s, T* v, int32_t*
   if (rc) return rc;
   if (batch < 0 || m < 0 || n < 0) return fail(BF_ERR_ARG, "negative batch or shape");
   if (m < n) return fail(BF_ERR_ARG, "svd requires m >= n, got %d x %d; pass the transpose", m, n);
-  if (o->accumulate_v && !v) return fail(BF_ERR_ARG, "accumulate_v set but v is NULL");
+  if (o->accumulate_v && !v && batch > 0 && n > 0) return fail(BF_ERR_ARG, "accumulate_v set but v is NULL");
   const bool f64 = sizeof(T) == 8;
   int dt = f64 ? 0 : 1;
   if (n == 0) {  // jacobi.py:244-249: empty result, converged, 0 sweeps
@@ -132,7 +132,8 @@ int block_impl(int64_t batch, int m, int n, const T* a, T* u, T* s, T* v, int32_
   if (rc) return rc;
   if (batch < 0 || m < 0 || n < 0) return fail(BF_ERR_ARG, "negative batch or shape");
   if (m < n) return fail(BF_ERR_ARG, "block_svd requires m >= n, got %d x %d", m, n);
-  if (o->accumulate_v && !v) return fail(BF_ERR_ARG, "accumulate_v set but v is NULL");
+  if (o->accumulate_v && !v && batch > 0 && n > 0) return fail(BF_ERR_ARG, "accumulate_v set but v is NULL");
+  if (batch == 0) return BF_OK;  // an empty batch maps to an empty result (core.py:97-123)
   if (!sweeps || !conv) return fail(BF_ERR_ARG, "sweeps and converged are required for block_svd");
   int k = o->block_width;
   if (o->method == 1) k = std::max(1, std::min(k, m / 2));

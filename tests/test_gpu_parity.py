@@ -222,6 +222,23 @@ def test_svd_errors():
     assert r.u.shape == (5, 0) and r.sigma.shape == (0,) and r.converged and r.sweeps == 0
 
 
+def test_empty_batches():
+    """Empty batches return empty results through every entry point (core.py:97-123: a batch
+    is a list; the reference maps over zero entries)."""
+    assert bf.batch_svd([]) == [] and bf.batch_qr([]) == [] and bf.batch_block_svd([]) == []
+    assert bf.batch_rsvd([], bf.RsvdOptions(k=2)) == []
+    z = torch.empty((0, 8, 6), dtype=torch.float64, device="cuda")
+    r = bf.svd_tensor(z, bf.JacobiOptions(accumulate_v=True))
+    assert r["u"].shape == (0, 8, 6) and r["sigma"].shape == (0, 6)
+    q, rr = bf.qr_tensor(z)
+    assert q.shape == (0, 8, 6) and rr.shape == (0, 6, 6)
+    z64 = torch.empty((0, 64, 64), dtype=torch.float64, device="cuda")
+    rb = bf.block_svd_tensor(z64, bf.BlockJacobiOptions(accumulate_v=True))
+    assert rb["sigma"].shape == (0, 64)
+    rs = bf.rsvd_tensor(z64, bf.RsvdOptions(k=8, p=8))
+    assert rs["s"].shape == (0, 16)
+
+
 # ------------------------------------------------------------------ block Jacobi
 
 
