@@ -163,9 +163,10 @@ def test_svd_batch_vs_oracle(shape, tier, ordering):
         assert vec_mismatch(v[b].T, o["v"][b].T, o["s"][b], np.float64) <= 1.0
 
 
-@pytest.mark.parametrize("shape", [(128, 122), (200, 100)])
+@pytest.mark.parametrize("shape", [(128, 122), (200, 100), (300, 180)])
 def test_svd_shared_tier_v_in_global(shape):
-    """Shapes whose W fits shared memory but W + V does not (W in smem, V in global/L2)."""
+    """Shapes whose W fits shared memory but W + V does not (W in smem, V in global/L2), and
+    one (300 x 180) where neither fits (everything in the global workspace)."""
     m, n = shape
     B = 6
     a = dev_gauss(B, m, n, 2_000_000 + m + n)
