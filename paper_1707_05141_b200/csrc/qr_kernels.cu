@@ -23,7 +23,10 @@ struct QrArgs {
 };
 
 template <typename T>
-__global__ void __launch_bounds__(256) qr_cta_kernel(QrArgs<T> a) {
+#ifndef BF_QRCTA_MAXW
+#define BF_QRCTA_MAXW 32  // 242x121: 1.83 -> 1.30 ms vs 8 warps
+#endif
+__global__ void __launch_bounds__(BF_QRCTA_MAXW * 32) qr_cta_kernel(QrArgs<T> a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int64_t b = blockIdx.x;
   if (b >= a.batch) return;
@@ -87,7 +90,7 @@ static int launch_qr_t(int64_t batch, int m, int n, const void* a, int64_t as, v
   p.gws = (T*)ws;
   p.gws_stride = (int64_t)((((size_t)m * n * sizeof(T) + 255) & ~(size_t)255) / sizeof(T));
   int nwarps = (n + 3) / 4;
-  nwarps = nwarps < 2 ? 2 : (nwarps > 8 ? 8 : nwarps);
+  nwarps = nwarps < 2 ? 2 : (nwarps > BF_QRCTA_MAXW ? BF_QRCTA_MAXW : nwarps);
   cudaError_t e = cudaFuncSetAttribute(qr_cta_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return (int)e;
   qr_cta_kernel<T><<<(unsigned)batch, nwarps * 32, smem, st>>>(p);
