@@ -96,7 +96,8 @@ BF_API int bf_block_svd_batched_f32(int64_t batch, int32_t m, int32_t n, const f
 
 /* ---- batched randomized SVD (Alg. 4): entry b uses seed ^ (index_base + b) (rsvd.py:79-86),
  * seed = seed_lo | seed_hi << 64. omega (nullable): batch x (n x (k+p)) sketch supplied by the
- * caller; NULL draws it on the device, bitwise equal to gaussian_matrix (f64 only).
+ * caller; NULL draws it on the device, bitwise equal to gaussian_matrix(n, k+p, seed ^ i, dtype)
+ * (rsvd.py:52,65: the f32 entry point draws numpy's float32 stream).
  * u: m x (k+p), s: k+p, v: n x (k+p) -- all k+p triplets, not truncated (rsvd.py:35-39). */
 BF_API size_t bf_rsvd_workspace_size(int64_t batch, int32_t m, int32_t n, int32_t k, int32_t p, int32_t dtype_bytes);
 BF_API int bf_rsvd_batched_f64(int64_t batch, int32_t m, int32_t n, int32_t k, int32_t p, uint64_t seed_lo,
@@ -110,6 +111,8 @@ BF_API int bf_rsvd_batched_f32(int64_t batch, int32_t m, int32_t n, int32_t k, i
  * when seed_mode == 0, (seed_lo + index_base + b, seed_hi) when seed_mode == 1. */
 BF_API int bf_gaussian_batched_f64(int64_t batch, int32_t rows, int32_t cols, uint64_t seed_lo, uint64_t seed_hi,
                             int64_t index_base, int32_t seed_mode, double* out, void* stream);
+BF_API int bf_gaussian_batched_f32(int64_t batch, int32_t rows, int32_t cols, uint64_t seed_lo, uint64_t seed_hi,
+                            int64_t index_base, int32_t seed_mode, float* out, void* stream);
 
 /* ---- testmat.make_matrix (testmat.py:83-94) on the device, geometric/arithmetic spectrum:
  * entry b uses seed_lo + index_base + b. Harness utility (input generation), not hot path. */

@@ -16,7 +16,7 @@
  *   _complete_zero_rows    jacobi.py:189-209      _extract_svd          jacobi.py:212-228
  *   svd                    jacobi.py:231-284      syrk                  core.py:68-78
  *   scaled_offdiag         blockjacobi.py:57-76   block_svd             blockjacobi.py:84-168
- *   gaussian_matrix        rsvd.py:42-53 (numpy 2.3.5 Philox4x64-10 + float64 ziggurat)
+ *   gaussian_matrix        rsvd.py:42-53 (numpy 2.3.5 Philox4x64-10 + float64 / float32 ziggurat)
  *   rsvd                   rsvd.py:56-76          batch_rsvd seed^i     rsvd.py:79-86
  *   spectrum / random_orthonormal / make_matrix   testmat.py:51-94
  *   batch_apply lowest-failing-index convention   core.py:97-123
@@ -141,6 +141,67 @@ static double orc_standard_normal(orc_philox* st) {
         return x;
     }
   }
+}
+
+/* numpy's next_uint32 on Philox (bit_generator buffering): the low half of a fresh 64-bit
+ * word, then its high half. */
+typedef struct {
+  orc_philox p;
+  int has32;
+  uint32_t hi32;
+} orc_philox32;
+
+static inline uint32_t orc_next_u32(orc_philox32* st) {
+  if (st->has32) {
+    st->has32 = 0;
+    return st->hi32;
+  }
+  uint64_t w = orc_philox_next(&st->p);
+  st->has32 = 1;
+  st->hi32 = (uint32_t)(w >> 32);
+  return (uint32_t)(w & 0xffffffffu);
+}
+
+static inline float orc_next_float(orc_philox32* st) {
+  return (float)(orc_next_u32(st) >> 8) * (1.0f / 16777216.0f);
+}
+
+/* numpy random_standard_normal_f (float32 ziggurat on 23-bit halves). log1pf is the C
+ * library's (npy_log1pf); the wedge test compares in double against exp(-0.5 x x). */
+static float orc_standard_normal_f(orc_philox32* st) {
+  for (;;) {
+    uint32_t r = orc_next_u32(st);
+    int idx = (int)(r & 0xff);
+    int sign = (int)((r >> 8) & 0x1);
+    uint32_t rabs = r >> 9;
+    float x = (float)rabs * bf_zig_wi_f[idx];
+    if (sign) x = -x;
+    if (rabs < bf_zig_ki_f[idx]) return x;
+    if (idx == 0) {
+      for (;;) {
+        float xx = -BF_ZIG_NOR_INV_R_F * log1pf(-orc_next_float(st));
+        float yy = -log1pf(-orc_next_float(st));
+        if (yy + yy > xx * xx) return ((rabs >> 8) & 0x1) ? -(BF_ZIG_NOR_R_F + xx) : BF_ZIG_NOR_R_F + xx;
+      }
+    } else {
+      if (((bf_zig_fi_f[idx - 1] - bf_zig_fi_f[idx]) * orc_next_float(st) + bf_zig_fi_f[idx]) <
+          exp(-0.5 * x * x))
+        return x;
+    }
+  }
+}
+
+/* gaussian_matrix(rows, cols, seed, dtype=float32) (rsvd.py:42-53, dtype=a.dtype at :65) */
+ORC_API int orc_gaussian_f32(int rows, int cols, uint64_t seed_lo, uint64_t seed_hi, float* out) {
+  if (rows < 0 || cols < 0) return -1;
+  orc_philox32 st;
+  memset(&st, 0, sizeof(st));
+  st.p.key[0] = seed_lo;
+  st.p.key[1] = seed_hi;
+  st.p.pos = 4;
+  for (int i = 0; i < rows; ++i)
+    for (int j = 0; j < cols; ++j) out[(size_t)j * rows + i] = orc_standard_normal_f(&st);
+  return 0;
 }
 
 /* gaussian_matrix(rows, cols, seed) (rsvd.py:42-53): C-order fill, returned column-major */

@@ -40,6 +40,7 @@ def lib():
         L = ctypes.CDLL(LIB_PATH)
         P, I, D, U64, I64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_double, ctypes.c_uint64, ctypes.c_int64
         L.orc_gaussian_f64.argtypes = [I, I, U64, U64, P]
+        L.orc_gaussian_f32.argtypes = [I, I, U64, U64, P]
         L.orc_philox_raw.argtypes = [U64, U64, I, P]
         L.orc_round_robin.argtypes = [I, P]
         L.orc_rotation.argtypes = [D, D, D, P]
@@ -93,10 +94,12 @@ def seed_split(seed):
     return seed & ((1 << 64) - 1), seed >> 64
 
 
-def gaussian_matrix(rows, cols, seed):
+def gaussian_matrix(rows, cols, seed, dtype=np.float64):
+    """rsvd.py:42-53: numpy's Philox standard_normal stream in `dtype` (float32 is its own stream)."""
     lo, hi = seed_split(seed)
-    out = np.empty((cols, rows), dtype=np.float64)
-    lib().orc_gaussian_f64(rows, cols, lo, hi, _p(out))
+    f32 = np.dtype(dtype) == np.float32
+    out = np.empty((cols, rows), dtype=np.float32 if f32 else np.float64)
+    (lib().orc_gaussian_f32 if f32 else lib().orc_gaussian_f64)(rows, cols, lo, hi, _p(out))
     return np.asfortranarray(out.T)
 
 

@@ -465,8 +465,11 @@ static int F(rsvd)(int m, int n, int kk, int p, uint64_t seed_lo, uint64_t seed_
   if (omega_in) {
     memcpy(omega, omega_in, sizeof(T) * (size_t)n * w);
   } else {
-    if (sizeof(T) != sizeof(double)) { free(omega); return -3; }
-    orc_gaussian_f64(n, w, seed_lo, seed_hi, (double*)omega);
+    /* the reference draws omega in the input's dtype (rsvd.py:65): float32 is its own stream */
+    if (sizeof(T) == sizeof(double))
+      orc_gaussian_f64(n, w, seed_lo, seed_hi, (double*)omega);
+    else
+      orc_gaussian_f32(n, w, seed_lo, seed_hi, (float*)omega);
   }
   T* y = (T*)malloc(sizeof(T) * (size_t)m * w);
   F(gemm_nn)(m, w, n, a, m, omega, n, y, m);

@@ -65,6 +65,7 @@ EXPORTS = (
     "bf_rsvd_batched_f64",
     "bf_rsvd_batched_f32",
     "bf_gaussian_batched_f64",
+    "bf_gaussian_batched_f32",
     "bf_make_matrix_workspace_size",
     "bf_make_matrix_batched_f64",
 )
@@ -120,8 +121,10 @@ def load():
         f = getattr(L, name)
         f.argtypes = [I64, I32, I32, I32, I32, U64, U64, I64, P, P, P, P, P, P, SZ, P]
         f.restype = ctypes.c_int
-    L.bf_gaussian_batched_f64.argtypes = [I64, I32, I32, U64, U64, I64, I32, P, P]
-    L.bf_gaussian_batched_f64.restype = ctypes.c_int
+    for name in ("bf_gaussian_batched_f64", "bf_gaussian_batched_f32"):
+        f = getattr(L, name)
+        f.argtypes = [I64, I32, I32, U64, U64, I64, I32, P, P]
+        f.restype = ctypes.c_int
     L.bf_make_matrix_workspace_size.argtypes = [I64, I32, I32]
     L.bf_make_matrix_workspace_size.restype = SZ
     L.bf_make_matrix_batched_f64.argtypes = [I64, I32, I32, I32, D, I32, U64, U64, I64, P, P, P, SZ, P]

@@ -202,8 +202,6 @@ int rsvd_impl(int64_t batch, int m, int n, int k, int p, uint64_t slo, uint64_t 
   if (w > std::min(m, n))  // rsvd.py:60-64
     return fail(BF_ERR_ARG, "k + p = %d exceeds min(m, n) = %d for shape (%d, ...)", w, std::min(m, n), m);
   const bool f64 = sizeof(T) == 8;
-  if (!omega && !f64)
-    return fail(BF_ERR_UNSUPPORTED, "float32 rsvd needs a caller-supplied omega (device float ziggurat not built)");
   const int es = sizeof(T), dt = f64 ? 0 : 1;
   RsvdLayout Ly = rsvd_layout(batch, m, n, w, es, omega == nullptr);
   int rc = check_ws(ws, wsb, Ly.total);
@@ -222,7 +220,9 @@ int rsvd_impl(int64_t batch, int m, int n, int k, int p, uint64_t slo, uint64_t 
   T* Vr = (T*)(base + Ly.vr);
   void* sws = base + Ly.svdws;
   if (!omega) {  // gaussian_matrix(n, w, seed ^ i) (rsvd.py:65, :82-85), kept in C order (row-major)
-    rc = bf::launch_gaussian_f64(batch, n, w, slo, shi, ibase, 0, 0, (double*)om, (int64_t)n * w, cs, 1);
+    // float32 inputs draw numpy's float32 stream (dtype=a.dtype), not a rounded float64 one
+    rc = f64 ? bf::launch_gaussian_f64(batch, n, w, slo, shi, ibase, 0, 0, (double*)om, (int64_t)n * w, cs, 1)
+             : bf::launch_gaussian_f32(batch, n, w, slo, shi, ibase, 0, 0, (float*)om, (int64_t)n * w, cs, 1);
     if (rc) return cuda_rc(rc, "rsvd/omega");
   }
   bf::GemmLaunch g;
@@ -373,6 +373,13 @@ int bf_gaussian_batched_f64(int64_t batch, int32_t rows, int32_t cols, uint64_t 
                             int32_t mode, double* out, void* st) {
   if (batch < 0 || rows < 0 || cols < 0) return fail(BF_ERR_ARG, "rows and cols must be >= 0");
   return cuda_rc(bf::launch_gaussian_f64(batch, rows, cols, slo, shi, ibase, mode, 0, out, (int64_t)rows * cols, S(st)),
+                 "gaussian");
+}
+
+int bf_gaussian_batched_f32(int64_t batch, int32_t rows, int32_t cols, uint64_t slo, uint64_t shi, int64_t ibase,
+                            int32_t mode, float* out, void* st) {
+  if (batch < 0 || rows < 0 || cols < 0) return fail(BF_ERR_ARG, "rows and cols must be >= 0");
+  return cuda_rc(bf::launch_gaussian_f32(batch, rows, cols, slo, shi, ibase, mode, 0, out, (int64_t)rows * cols, S(st)),
                  "gaussian");
 }
 

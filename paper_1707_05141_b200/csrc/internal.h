@@ -67,6 +67,9 @@ int launch_gemm(int dtype, const GemmLaunch& L, cudaStream_t st);
 int launch_gaussian_f64(int64_t batch, int rows, int cols, uint64_t seed_lo, uint64_t seed_hi, int64_t index_base,
                         int seed_mode, uint64_t xor_mask, double* out, int64_t out_stride, cudaStream_t st,
                         int c_order = 0);
+int launch_gaussian_f32(int64_t batch, int rows, int cols, uint64_t seed_lo, uint64_t seed_hi, int64_t index_base,
+                        int seed_mode, uint64_t xor_mask, float* out, int64_t out_stride, cudaStream_t st,
+                        int c_order = 0);
 int launch_sign_fix_f64(int64_t batch, int m, int n, double* q, const double* r, cudaStream_t st);
 int launch_scale_cols_f64(int64_t batch, int m, int n, double* q, const double* sigma, cudaStream_t st);
 

@@ -4,6 +4,7 @@
 
 #define BF_ZIG_QUAL static __device__ const
 #include "ziggurat_tables.h"
+#include "libm_log1p.h"
 
 namespace bf {
 
@@ -241,13 +242,22 @@ int launch_gemm(int dtype, const GemmLaunch& g, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ Gaussian sampler
-// numpy Generator(Philox(key=seed)).standard_normal((rows, cols)) (rsvd.py:42-53):
-// Philox4x64-10 stream (counter incremented before each 4-word block), float64
-// ziggurat (numpy random_standard_normal), C-order fill.
-// One warp per matrix: each lane computes one Philox block (4 consecutive stream words), so a
-// warp tests 128 words against the ziggurat fast path at once; accepted samples are compacted
-// by a warp prefix sum and stored contiguously (C order) or transposed (column-major). The rare
-// slow path (~1.2% of words: wedge / tail) is walked by lane 0 and the warp resumes after it.
+// numpy Generator(Philox(key=seed)).standard_normal((rows, cols), dtype) (rsvd.py:42-53; the
+// reference passes dtype=a.dtype, rsvd.py:65): Philox4x64-10 stream (counter incremented before
+// each 4-word block), C-order fill, and numpy's ziggurat for the dtype:
+//   float64: random_standard_normal   -- one 64-bit word per draw, 52-bit rabs;
+//   float32: random_standard_normal_f -- one 32-bit draw per try (next_uint32: the low half of a
+//            word, then its high half), 23-bit rabs, float tables, double-precision wedge test.
+// Bitwise equal to numpy: the tables are numpy's own (tools/gen_ziggurat_tables.py), every
+// operation is an explicitly rounded IEEE op in numpy's order (no FMA contraction), and the tail
+// uses log1p/log1pf restated from the host libm (libm_log1p.h). The wedge's exp() only decides
+// accept/reject: CUDA's and glibc's exp differ by <= 1-2 ulp, which flips the decision only if
+// the left side lands inside that ulp window (probability ~1e-14 per wedge event).
+//
+// One warp per matrix: each lane computes one Philox block (4 words = D draws), so a warp tests
+// 32 D draws against the ziggurat fast path at once; accepted samples are compacted by a warp
+// prefix sum and stored contiguously (C order) or transposed (column-major). The rare slow path
+// (wedge / tail: ~1.2% of f64 draws) is walked by lane 0 and the warp resumes after it.
 
 BF_DEV void philox_block(uint64_t k0, uint64_t k1, uint64_t blk, uint64_t (&w)[4]) {
   uint64_t c0 = blk + 1, c1 = 0, c2 = 0, c3 = 0;
@@ -281,20 +291,124 @@ BF_DEV uint64_t philox_word(uint64_t k0, uint64_t k1, uint64_t pos) {
   }
 }
 
-BF_DEV double u01(uint64_t r) { return (double)(r >> 11) * (1.0 / 9007199254740992.0); }
+template <typename T>
+struct Zig;
 
+template <>
+struct Zig<double> {
+  using U = uint64_t;
+  static constexpr int D = 4;  // draws per Philox block
+  static BF_DEV void split(const uint64_t (&w)[4], U (&d)[D]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) d[q] = w[q];
+  }
+  static BF_DEV U draw(uint64_t k0, uint64_t k1, uint64_t p) { return philox_word(k0, k1, p); }
+  static BF_DEV double uni(U r) { return __dmul_rn((double)(r >> 11), 1.0 / 9007199254740992.0); }  // next_double
+  // fast path: x = rabs * wi[idx] (sign from bit 8), accepted iff rabs < ki[idx]
+  static BF_DEV bool fast(U r, double& x) {
+    const int idx = (int)(r & 0xff);
+    const uint64_t rabs = (r >> 9) & 0x000fffffffffffffULL;
+    const double v = __dmul_rn((double)rabs, bf_zig_wi[idx]);
+    x = ((r >> 8) & 1) ? -v : v;
+    return rabs < bf_zig_ki[idx];
+  }
+  // slow path of draw r (numpy random_standard_normal after the fast test fails); the next draw
+  // is `nxt` when the caller has it (has_nxt), else read from the stream at p. Advances p.
+  static BF_DEV bool slow(U r, U nxt, bool has_nxt, uint64_t k0, uint64_t k1, uint64_t& p, double& val) {
+    const int idx = (int)(r & 0xff);
+    const uint64_t rabs = (r >> 9) & 0x000fffffffffffffULL;
+    double xs = __dmul_rn((double)rabs, bf_zig_wi[idx]);
+    if ((r >> 8) & 1) xs = -xs;
+    if (idx == 0) {
+      for (;;) {
+        const double xx = __dmul_rn(-BF_ZIG_NOR_INV_R, bf_libm::log1p_d(-uni(draw(k0, k1, p))));
+        const double yy = -bf_libm::log1p_d(-uni(draw(k0, k1, p + 1)));
+        p += 2;
+        if (__dadd_rn(yy, yy) > __dmul_rn(xx, xx)) {
+          const double t = __dadd_rn(xx, BF_ZIG_NOR_R);
+          val = ((rabs >> 8) & 0x1) ? -t : t;
+          return true;
+        }
+      }
+    }
+    const double u = uni(has_nxt ? nxt : draw(k0, k1, p));
+    p += 1;
+    const double lhs = __dadd_rn(__dmul_rn(__dsub_rn(bf_zig_fi[idx - 1], bf_zig_fi[idx]), u), bf_zig_fi[idx]);
+    val = xs;
+    return lhs < exp(__dmul_rn(__dmul_rn(-0.5, xs), xs));
+  }
+};
+
+template <>
+struct Zig<float> {
+  using U = uint32_t;
+  static constexpr int D = 8;
+  static BF_DEV void split(const uint64_t (&w)[4], U (&d)[D]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      d[2 * q] = (uint32_t)(w[q] & 0xffffffffu);
+      d[2 * q + 1] = (uint32_t)(w[q] >> 32);
+    }
+  }
+  static BF_DEV U draw(uint64_t k0, uint64_t k1, uint64_t p) {
+    const uint64_t w = philox_word(k0, k1, p >> 1);
+    return (p & 1) ? (uint32_t)(w >> 32) : (uint32_t)(w & 0xffffffffu);
+  }
+  static BF_DEV float uni(U r) { return __fmul_rn((float)(r >> 8), 1.0f / 16777216.0f); }  // next_float
+  static BF_DEV bool fast(U r, float& x) {
+    const int idx = (int)(r & 0xff);
+    const uint32_t rabs = r >> 9;
+    const float v = __fmul_rn((float)rabs, bf_zig_wi_f[idx]);
+    x = ((r >> 8) & 1) ? -v : v;
+    return rabs < bf_zig_ki_f[idx];
+  }
+  static BF_DEV bool slow(U r, U nxt, bool has_nxt, uint64_t k0, uint64_t k1, uint64_t& p, float& val) {
+    const int idx = (int)(r & 0xff);
+    const uint32_t rabs = r >> 9;
+    float xs = __fmul_rn((float)rabs, bf_zig_wi_f[idx]);
+    if ((r >> 8) & 1) xs = -xs;
+    if (idx == 0) {
+      for (;;) {
+        const float xx = __fmul_rn(-BF_ZIG_NOR_INV_R_F, bf_libm::log1p_f(-uni(draw(k0, k1, p))));
+        const float yy = -bf_libm::log1p_f(-uni(draw(k0, k1, p + 1)));
+        p += 2;
+        if (__fadd_rn(yy, yy) > __fmul_rn(xx, xx)) {
+          const float t = __fadd_rn(xx, BF_ZIG_NOR_R_F);
+          val = ((rabs >> 8) & 0x1) ? -t : t;
+          return true;
+        }
+      }
+    }
+    const float u = uni(has_nxt ? nxt : draw(k0, k1, p));
+    p += 1;
+    const float lhs = __fadd_rn(__fmul_rn(u, __fsub_rn(bf_zig_fi_f[idx - 1], bf_zig_fi_f[idx])), bf_zig_fi_f[idx]);
+    val = xs;
+    const double xd = (double)xs;
+    return (double)lhs < exp(__dmul_rn(__dmul_rn(-0.5, xd), xd));
+  }
+};
+
+template <typename T>
+BF_DEV typename Zig<T>::U shfl_draw(typename Zig<T>::U v, int src) {
+  return __shfl_sync(FULL, v, src);
+}
+
+template <typename T>
 __global__ void gaussian_kernel(int64_t batch, int rows, int cols, uint64_t seed_lo, uint64_t seed_hi,
-                                int64_t index_base, int seed_mode, uint64_t xor_mask, double* out,
-                                int64_t out_stride, int c_order) {
+                                int64_t index_base, int seed_mode, uint64_t xor_mask, T* out, int64_t out_stride,
+                                int c_order) {
+  using Z = Zig<T>;
+  using U = typename Z::U;
+  constexpr int D = Z::D;
   const int lane = threadIdx.x & 31;
   const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (b >= batch) return;
   uint64_t gi = (uint64_t)(index_base + b);
   const uint64_t k0 = (seed_mode == 0 ? (seed_lo ^ gi) : (seed_lo + gi)) ^ xor_mask;
   const uint64_t k1 = seed_hi;
-  double* o = out + b * out_stride;
+  T* o = out + b * out_stride;
   const int64_t total = (int64_t)rows * cols;
-  auto store = [&](int64_t kk, double v) {
+  auto store = [&](int64_t kk, T v) {
     if (kk < total) {
       if (c_order)
         o[kk] = v;
@@ -303,98 +417,71 @@ __global__ void gaussian_kernel(int64_t batch, int rows, int cols, uint64_t seed
     }
   };
   int64_t k = 0;
-  uint64_t pos = 0;
+  uint64_t pos = 0;  // stream position in draws
   while (k < total) {
-    // one batch: lane l holds stream words 4 (blk + l) .. 4 (blk + l) + 3
-    const uint64_t blk = pos >> 2;
-    const uint64_t bend = (blk + 32) * 4;
+    // one batch: lane l holds draws D (blk + l) .. D (blk + l) + D - 1
+    const uint64_t blk = pos / D;
+    const uint64_t bend = (blk + 32) * D;
     uint64_t w[4];
     philox_block(k0, k1, blk + lane, w);
-    double x[4];
-    bool fast[4];
+    U d[D];
+    Z::split(w, d);
+    T x[D];
+    bool fast[D];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint64_t r = w[q];
-      const int idx = (int)(r & 0xff);
-      const uint64_t rr = r >> 8;
-      const uint64_t rabs = (rr >> 1) & 0x000fffffffffffffULL;
-      const double v = (double)rabs * bf_zig_wi[idx];
-      x[q] = (rr & 1) ? -v : v;
-      fast[q] = rabs < bf_zig_ki[idx];
-    }
+    for (int q = 0; q < D; ++q) fast[q] = Z::fast(d[q], x[q]);
     // the batch is consumed from `pos` on; every slow-path event is resolved inside it (its
-    // extra words come from the batch's registers when they lie in it), so Philox runs once
-    // per 128 words instead of once per event
+    // extra draws come from the batch's registers when they lie in it), so Philox runs once
+    // per 32 D draws instead of once per event
     while (k < total && pos < bend) {
-      const uint64_t lane0 = (blk + lane) * 4;  // stream position of this lane's word 0
-      int rej = 4;
-      int first = 4;  // first unconsumed word of this lane
+      const uint64_t lane0 = (blk + lane) * D;  // stream position of this lane's draw 0
+      int rej = D;
+      int first = D;  // first unconsumed draw of this lane
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < D; ++q) {
         const bool live = lane0 + q >= pos;
-        first = (live && first == 4) ? q : first;
-        if (live && rej == 4 && !fast[q]) rej = q;
+        first = (live && first == D) ? q : first;
+        if (live && rej == D && !fast[q]) rej = q;
       }
-      const unsigned bal = __ballot_sync(FULL, rej < 4);
+      const unsigned bal = __ballot_sync(FULL, rej < D);
       const int L = bal ? __ffs(bal) - 1 : 32;
-      const int cnt = lane < L ? 4 - first : (lane == L ? rej - first : 0);
+      const int cnt = lane < L ? D - first : (lane == L ? rej - first : 0);
       int incl = cnt;
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int y = __shfl_up_sync(FULL, incl, d);
-        if (lane >= d) incl += y;
+      for (int dd = 1; dd < 32; dd <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, dd);
+        if (lane >= dd) incl += y;
       }
       const int start = incl - cnt;
       const int tot = __shfl_sync(FULL, incl, 31);
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < D; ++q)
         if (q >= first && q - first < cnt) store(k + start + (q - first), x[q]);
       k += tot;
       if (L == 32) {
         pos = bend;
         break;
       }
-      // slow path for the first failing word (lane L, word q_s) at stream position ps
+      // slow path for the first failing draw (lane L, draw q_s) at stream position ps
       const int q_s = __shfl_sync(FULL, rej, L);
-      uint64_t r_s = w[0];
+      U r_s = d[0];
 #pragma unroll
-      for (int q = 1; q < 4; ++q) r_s = q == q_s ? w[q] : r_s;
-      r_s = __shfl_sync(FULL, r_s, L);
-      uint64_t p = (blk + L) * 4 + q_s + 1;
-      // the wedge test's uniform is the next word: from the batch when it is in it
-      const int lw = (int)((p >> 2) - blk), qw = (int)(p & 3);
-      uint64_t r_u = w[0];
+      for (int q = 1; q < D; ++q) r_s = q == q_s ? d[q] : r_s;
+      r_s = shfl_draw<T>(r_s, L);
+      uint64_t p = (blk + L) * D + q_s + 1;
+      // the wedge test's uniform is the next draw: from the batch when it is in it
+      const int lw = (int)(p / D - blk), qw = (int)(p % D);
+      U r_u = d[0];
 #pragma unroll
-      for (int q = 1; q < 4; ++q) r_u = q == qw ? w[q] : r_u;
-      r_u = __shfl_sync(FULL, r_u, lw < 32 ? lw : 0);
+      for (int q = 1; q < D; ++q) r_u = q == qw ? d[q] : r_u;
+      r_u = shfl_draw<T>(r_u, lw < 32 ? lw : 0);
       int produced = 0;
       if (lane == 0 && k < total) {
-        const int idx_s = (int)(r_s & 0xff);
-        const uint64_t rr = r_s >> 8;
-        const uint64_t rabs_s = (rr >> 1) & 0x000fffffffffffffULL;
-        double xs = (double)rabs_s * bf_zig_wi[idx_s];
-        if (rr & 1) xs = -xs;
-        double val = 0.0;
-        if (idx_s == 0) {
-          for (;;) {
-            double xx = -BF_ZIG_NOR_INV_R * log1p(-u01(philox_word(k0, k1, p)));
-            double yy = -log1p(-u01(philox_word(k0, k1, p + 1)));
-            p += 2;
-            if (yy + yy > xx * xx) {
-              val = ((rabs_s >> 8) & 0x1) ? -(BF_ZIG_NOR_R + xx) : BF_ZIG_NOR_R + xx;
-              produced = 1;
-              break;
-            }
-          }
-        } else {
-          const double u = u01(lw < 32 ? r_u : philox_word(k0, k1, p));
-          p += 1;
-          if (((bf_zig_fi[idx_s - 1] - bf_zig_fi[idx_s]) * u + bf_zig_fi[idx_s]) < exp(-0.5 * xs * xs)) {
-            val = xs;
-            produced = 1;
-          }
+        T val;
+        if (Z::slow(r_s, r_u, lw < 32, k0, k1, p, val)) {
+          store(k, val);
+          produced = 1;
         }
-        if (produced) store(k, val);
       }
       produced = __shfl_sync(FULL, produced, 0);
       p = __shfl_sync(FULL, p, 0);
@@ -404,15 +491,29 @@ __global__ void gaussian_kernel(int64_t batch, int rows, int cols, uint64_t seed
   }
 }
 
-int launch_gaussian_f64(int64_t batch, int rows, int cols, uint64_t seed_lo, uint64_t seed_hi, int64_t index_base,
-                        int seed_mode, uint64_t xor_mask, double* out, int64_t out_stride, cudaStream_t st,
-                        int c_order) {
+template <typename T>
+int launch_gaussian(int64_t batch, int rows, int cols, uint64_t seed_lo, uint64_t seed_hi, int64_t index_base,
+                    int seed_mode, uint64_t xor_mask, T* out, int64_t out_stride, cudaStream_t st, int c_order) {
   if (batch == 0 || rows == 0 || cols == 0) return 0;
   const int wpb = 4;
   unsigned grid = (unsigned)((batch + wpb - 1) / wpb);
-  gaussian_kernel<<<grid, wpb * 32, 0, st>>>(batch, rows, cols, seed_lo, seed_hi, index_base, seed_mode, xor_mask,
-                                               out, out_stride, c_order);
+  gaussian_kernel<T><<<grid, wpb * 32, 0, st>>>(batch, rows, cols, seed_lo, seed_hi, index_base, seed_mode,
+                                                  xor_mask, out, out_stride, c_order);
   return (int)cudaGetLastError();
+}
+
+int launch_gaussian_f64(int64_t batch, int rows, int cols, uint64_t seed_lo, uint64_t seed_hi, int64_t index_base,
+                        int seed_mode, uint64_t xor_mask, double* out, int64_t out_stride, cudaStream_t st,
+                        int c_order) {
+  return launch_gaussian<double>(batch, rows, cols, seed_lo, seed_hi, index_base, seed_mode, xor_mask, out,
+                                 out_stride, st, c_order);
+}
+
+int launch_gaussian_f32(int64_t batch, int rows, int cols, uint64_t seed_lo, uint64_t seed_hi, int64_t index_base,
+                        int seed_mode, uint64_t xor_mask, float* out, int64_t out_stride, cudaStream_t st,
+                        int c_order) {
+  return launch_gaussian<float>(batch, rows, cols, seed_lo, seed_hi, index_base, seed_mode, xor_mask, out,
+                                out_stride, st, c_order);
 }
 
 // random_orthonormal sign fix (testmat.py:68-80): flip column j where R_jj < 0.

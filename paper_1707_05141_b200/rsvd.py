@@ -1,9 +1,10 @@
 """Batched randomized SVD (reference: /root/reference/pkg/src/batchfact/rsvd.py).
 
 ``RsvdOptions`` / ``TruncatedSvd`` (rsvd.py:19-39), ``gaussian_matrix`` (rsvd.py:42-53,
-numpy Philox4x64-10 + float64 ziggurat, reproduced bit-for-bit on the device),
-``rsvd`` (Alg. 4, rsvd.py:56-76) and ``batch_rsvd`` with per-entry seed ``seed ^ i``
-(rsvd.py:79-86). Computation: ``bf_rsvd_batched_*`` / ``bf_gaussian_batched_f64``.
+numpy Philox4x64-10 + the float64 or float32 ziggurat, reproduced bit-for-bit on the device),
+``rsvd`` (Alg. 4, rsvd.py:56-76; the sketch is drawn in the input's dtype, rsvd.py:65) and
+``batch_rsvd`` with per-entry seed ``seed ^ i`` (rsvd.py:79-86).
+Computation: ``bf_rsvd_batched_*`` / ``bf_gaussian_batched_*``.
 """
 
 from dataclasses import dataclass
@@ -58,29 +59,34 @@ def split_seed(seed):
     return key & _M64, key >> 64
 
 
-def gaussian_tensor(batch, rows, cols, seed, *, index_base=0, seed_mode="xor", device=None):
-    """(batch, rows, cols) float64 CUDA tensor; entry b is gaussian_matrix(rows, cols, key_b)
-    with key_b = seed ^ (index_base + b) (seed_mode "xor") or seed + index_base + b ("add")."""
+def gaussian_tensor(batch, rows, cols, seed, *, index_base=0, seed_mode="xor", dtype=torch.float64, device=None):
+    """(batch, rows, cols) CUDA tensor; entry b is gaussian_matrix(rows, cols, key_b, dtype) with
+    key_b = seed ^ (index_base + b) (seed_mode "xor") or seed + index_base + b ("add").
+    float32 is numpy's float32 stream (its own ziggurat), not a rounded float64 draw."""
     if rows < 0 or cols < 0:
         raise ValueError("rows and cols must be >= 0")
+    if dtype not in (torch.float64, torch.float32):
+        raise ValueError(f"dtype must be float64 or float32, got {dtype}")
     L = _lib.load()
     dev = resolve_device(device)
     lo, hi = split_seed(seed)
-    out = torch.empty((batch, cols, rows), dtype=torch.float64, device=dev)
+    out = torch.empty((batch, cols, rows), dtype=dtype, device=dev)
+    fn = L.bf_gaussian_batched_f64 if dtype == torch.float64 else L.bf_gaussian_batched_f32
     with torch.cuda.device(dev):
-        rc = L.bf_gaussian_batched_f64(batch, rows, cols, lo, hi, index_base, 0 if seed_mode == "xor" else 1, ptr(out),
-                                       stream_handle(dev))
+        rc = fn(batch, rows, cols, lo, hi, index_base, 0 if seed_mode == "xor" else 1, ptr(out), stream_handle(dev))
     _lib.check(rc, "gaussian")
     return from_colmajor(out)
 
 
 def gaussian_matrix(rows, cols, seed, dtype=np.float64, *, device=None):
-    """I.i.d. standard normal matrix, bitwise equal to the reference's (rsvd.py:42-53)."""
+    """I.i.d. standard normal matrix, bitwise equal to the reference's (rsvd.py:42-53) in
+    float64 or float32 (numpy draws float32 with its own float ziggurat)."""
     if rows < 0 or cols < 0:
         raise ValueError("rows and cols must be >= 0")
-    if np.dtype(dtype) != np.float64:
-        raise NotImplementedError("the float32 ziggurat stream is not built on the device (float64 only)")
-    t = gaussian_tensor(1, rows, cols, seed, device=device)
+    dt = np.dtype(dtype)
+    if dt not in (np.float64, np.float32):
+        raise ValueError(f"dtype must be float64 or float32, got {dt}")
+    t = gaussian_tensor(1, rows, cols, seed, dtype=torch_dtype(dt), device=device)
     return np.asfortranarray(to_host(colmajor(t))[0].T)
 
 
@@ -118,7 +124,18 @@ def rsvd_tensor(a, opts, *, index_base=0, omega=None):
     check_batched_tensor(a, "rsvd_tensor")
     B, m, n = a.shape
     _check_width(m, n, opts)
-    om = None if omega is None else colmajor(omega.to(a.dtype))
+    om = None
+    if omega is not None:
+        # the kernels read n (k+p) entries per matrix at a fixed stride: validate before the launch
+        w = opts.k + opts.p
+        if not isinstance(omega, torch.Tensor) or tuple(omega.shape) != (B, n, w):
+            raise ValueError(f"omega must be a ({B}, {n}, {w}) tensor, got "
+                             f"{tuple(omega.shape) if isinstance(omega, torch.Tensor) else type(omega).__name__}")
+        if omega.device != a.device:
+            raise ValueError(f"omega is on {omega.device}, a is on {a.device}")
+        if omega.dtype != a.dtype:
+            raise ValueError(f"omega dtype {omega.dtype} differs from a's {a.dtype}")
+        om = colmajor(omega)
     r = rsvd_colmajor(colmajor(a), m, n, opts, index_base=index_base, omega_store=om)
     return dict(u=from_colmajor(r["u"]), s=r["s"], v=from_colmajor(r["v"]))
 
@@ -133,9 +150,6 @@ def batch_rsvd(batch, opts, *, threads=1, device=None):
         try:
             a = as_matrix(e)
             _check_width(a.shape[0], a.shape[1], opts)
-            if a.dtype != np.float64:
-                raise NotImplementedError("float32 rsvd draws its sketch with numpy's float32 ziggurat; "
-                                          "pass omega through rsvd_tensor")
             mats.append(a)
         except Exception as exc:  # noqa: BLE001
             errors[i] = exc
@@ -148,7 +162,7 @@ def batch_rsvd(batch, opts, *, threads=1, device=None):
     i = 0
     while i < len(mats):
         j = i
-        while j + 1 < len(mats) and mats[j + 1].shape == mats[i].shape:
+        while j + 1 < len(mats) and mats[j + 1].shape == mats[i].shape and mats[j + 1].dtype == mats[i].dtype:
             j += 1
         m, n = mats[i].shape
         host = torch.empty((j - i + 1, n, m), dtype=torch_dtype(mats[i].dtype), pin_memory=True)

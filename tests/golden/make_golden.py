@@ -173,6 +173,9 @@ def gen_rsvd():
     r8 = gauss(50, 8, 5_100_001) @ gauss(8, 30, 5_100_002)
     cases.append(("rank8_50x30", r8, 8, 4, 3, 0, None))
     cases.append(("diag", np.diag(10.0 ** -np.arange(10.0)), 4, 3, 0, 0, None))
+    # float32 input: the reference draws its sketch in float32 (rsvd.py:65, dtype=a.dtype)
+    a32, _ = testmat.make_matrix(64, testmat.SpectrumSpec(n=48, mode="geometric", cond=1e6, rank=48), 5_100_003)
+    cases.append(("f32_64x48", a32.astype(np.float32), 8, 4, 11, 3, None))
     out = {"names": np.array([c[0] for c in cases])}
     for name, a, k, p, seed, index, sig in cases:
         a = np.asfortranarray(a)
@@ -192,6 +195,8 @@ def gen_gauss_testmat():
         out[f"g{j}/seed_lo"] = np.uint64(s & ((1 << 64) - 1))
         out[f"g{j}/seed_hi"] = np.uint64(s >> 64)
         out[f"g{j}/x"] = gauss(128, 40, s)
+        # float32 is numpy's own float ziggurat stream (rsvd.py:52 with dtype=float32)
+        out[f"g{j}/x32"] = gauss(128, 40, s, np.float32)
     out["g_count"] = len(seeds)
     spec = testmat.SpectrumSpec(n=128, mode="geometric", cond=1e16, rank=64)
     a, sig = testmat.make_matrix(128, spec, 5_000_000)
@@ -207,7 +212,10 @@ def gen_gauss_testmat():
 
 
 if __name__ == "__main__":
+    only = set(sys.argv[1:])  # e.g. `make_golden.py gen_rsvd` regenerates one fixture file
     for fn in (gen_gauss_testmat, gen_qr, gen_svd, gen_rsvd, gen_block):
+        if only and fn.__name__ not in only:
+            continue
         t0 = time.time()
         fn()
         print(f"{fn.__name__}: {time.time() - t0:.1f}s")

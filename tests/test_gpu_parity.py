@@ -41,27 +41,44 @@ def stack_np(t):
 
 
 def test_gaussian_bitwise_vs_reference():
+    """gaussian_matrix == the reference's own draws (golden), bit for bit, float64 and float32."""
     g = golden("gauss_testmat")
     for j in range(int(g["g_count"])):
         seed = int(g[f"g{j}/seed_lo"]) | (int(g[f"g{j}/seed_hi"]) << 64)
         x = bf.gaussian_matrix(128, 40, seed)
-        ref = g[f"g{j}/x"]
-        # bit-exact except possibly the rare ziggurat tail samples (log1p ulp); count them
-        diff = x != ref
-        assert np.sum(diff) <= 1, f"seed {seed}: {np.sum(diff)} mismatches"
-        if np.any(diff):
-            assert np.max(np.abs(x[diff] - ref[diff]) / np.abs(ref[diff])) < 4e-16
+        assert x.dtype == np.float64 and np.array_equal(x, g[f"g{j}/x"]), f"f64 seed {seed}"
+        x32 = bf.gaussian_matrix(128, 40, seed, np.float32)
+        assert x32.dtype == np.float32 and np.array_equal(x32, g[f"g{j}/x32"]), f"f32 seed {seed}"
 
 
-def test_gaussian_batch_matches_oracle():
-    t = bf.gaussian_tensor(64, 128, 40, 5, seed_mode="xor")
-    got = stack_np(t)
-    mism = 0
-    for b in range(64):
-        ref = orc.gaussian_matrix(128, 40, 5 ^ b)
-        mism += int(np.sum(got[b].T != ref))
-        assert np.allclose(got[b].T, ref, rtol=1e-15, atol=0)
-    assert mism <= 8
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_gaussian_batch_bitwise_vs_oracle(dtype):
+    """10^4 cfg5 sketches (128 x 40, keys 5 ^ i) against the oracle (numpy's stream restated in C,
+    pinned to numpy above): array_equal. ~1.3 ziggurat-tail samples per matrix, so the tail
+    (log1p) and wedge paths are exercised thousands of times; asserted below."""
+    B = 10_000
+    t = bf.gaussian_tensor(B, 128, 40, 5, seed_mode="xor", dtype=dtype)
+    got = stack_np(t)  # (B, 40, 128): per-matrix column-major
+    npd = np.float64 if dtype == torch.float64 else np.float32
+    ref = np.stack([orc.gaussian_matrix(128, 40, 5 ^ b, npd).T for b in range(B)])
+    assert got.dtype == ref.dtype
+    bad = np.flatnonzero(np.any(got != ref, axis=(1, 2)))
+    assert bad.size == 0, f"{bad.size} matrices differ, first {bad[:8]}"
+    tails = int(np.sum(np.abs(got) > 3.6541528853610088))  # ziggurat tail samples exceed r
+    assert tails > 5000, tails
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_gaussian_long_streams_bitwise(dtype):
+    """Long streams (Philox block boundaries, many slow-path events per matrix), C-order and
+    column-major stores, 128-bit keys."""
+    npd = np.float64 if dtype == torch.float64 else np.float32
+    for seed in (0, (1 << 64) + 9, (1 << 127) + 12345):
+        t = bf.gaussian_tensor(2, 700, 301, seed, seed_mode="add", dtype=dtype)
+        got = stack_np(t)
+        for b in range(2):
+            ref = orc.gaussian_matrix(700, 301, seed + b, npd)
+            assert np.array_equal(got[b].T, ref), (seed, b)
 
 
 # ------------------------------------------------------------------ QR
@@ -356,7 +373,8 @@ def test_rsvd_golden(nm):
     a = c["a"]
     seed = int(c["seed"]) ^ int(c["index"])
     r = bf.rsvd(a, bf.RsvdOptions(k=int(c["k"]), p=int(c["p"]), seed=seed))
-    assert sigma_normwise(r.s, c["s"]) <= 1e-12
+    assert r.s.dtype == a.dtype
+    assert sigma_normwise(r.s, c["s"]) <= gate(a.dtype)
     k = int(c["k"])
     assert vec_mismatch(r.u[:, :k], c["u"][:, :k], c["s"][:k], a.dtype, factor=4096.0) <= 1.0
     assert vec_mismatch(r.v[:, :k], c["v"][:, :k], c["s"][:k], a.dtype, factor=4096.0) <= 1.0
@@ -378,6 +396,31 @@ def test_rsvd_f32_with_caller_omega_vs_oracle():
     u = r["u"].cpu().double()
     orth = (u.transpose(1, 2) @ u - torch.eye(k + p, dtype=torch.float64)).abs().max()
     assert float(orth) < 1e-4
+
+
+def test_rsvd_f32_device_omega_vs_oracle():
+    """f32 rsvd drawing its own sketch on the device -- numpy's float32 stream, as the reference
+    does for float32 input (rsvd.py:65) -- against the oracle (same stream, drawn in C)."""
+    B, m, n, k, p = 64, 96, 80, 16, 8
+    a64, _ = bf.make_matrix_tensor(B, m, n, 1e5, rank=n, seed=5_200_000)
+    a = a64.float()
+    r = bf.rsvd_tensor(a, bf.RsvdOptions(k=k, p=p, seed=21), index_base=7)
+    o = orc.batch_rsvd_stacked(stack_np(a), m, n, k, p, seed=21, index_base=7, threads=8)
+    s = r["s"].cpu().numpy()
+    assert s.dtype == np.float32
+    for b in range(B):
+        assert sigma_normwise(s[b], o["s"][b]) <= 1e-5
+
+
+def test_rsvd_omega_validation():
+    a = torch.randn(4, 32, 24, dtype=torch.float64, device="cuda")
+    opts = bf.RsvdOptions(k=4, p=2)
+    with pytest.raises(ValueError):
+        bf.rsvd_tensor(a, opts, omega=torch.randn(4, 24, 4, dtype=torch.float64, device="cuda"))  # k, not k+p
+    with pytest.raises(ValueError):
+        bf.rsvd_tensor(a, opts, omega=torch.randn(4, 24, 6, dtype=torch.float64))  # host tensor
+    with pytest.raises(ValueError):
+        bf.rsvd_tensor(a, opts, omega=torch.randn(4, 24, 6, dtype=torch.float32, device="cuda"))
 
 
 def test_rsvd_cfg5_batch_vs_oracle():

@@ -79,6 +79,8 @@ def test_gaussian_bit_exact():
         seed = int(g[f"g{j}/seed_lo"]) | (int(g[f"g{j}/seed_hi"]) << 64)
         x = orc.gaussian_matrix(128, 40, seed)
         assert np.array_equal(x, g[f"g{j}/x"]), f"seed {seed}"
+        x32 = orc.gaussian_matrix(128, 40, seed, np.float32)
+        assert x32.dtype == np.float32 and np.array_equal(x32, g[f"g{j}/x32"]), f"f32 seed {seed}"
 
 
 def test_philox_raw_matches_numpy():
@@ -192,7 +194,7 @@ def test_rsvd_matches_reference(nm):
     seed = int(c["seed"]) ^ int(c["index"])
     r = orc.rsvd(a, int(c["k"]), int(c["p"]), seed)
     assert r["bad"] == -1
-    assert sigma_normwise(r["s"], c["s"]) <= 1e-12
+    assert sigma_normwise(r["s"], c["s"]) <= (1e-12 if a.dtype == np.float64 else 1e-5)
     k = int(c["k"])
     assert vec_mismatch(r["u"][:, :k], c["u"][:, :k], c["s"][:k], a.dtype, factor=4096.0) <= 1.0
     assert vec_mismatch(r["v"][:, :k], c["v"][:, :k], c["s"][:k], a.dtype, factor=4096.0) <= 1.0
