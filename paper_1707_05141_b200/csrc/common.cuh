@@ -31,13 +31,19 @@ BF_DEV T warp_allreduce_max(T v) {
   return v;
 }
 
-// Fast reciprocal / reciprocal square root: MUFU seed + 2 Newton steps (~1 ulp).
+// Fast reciprocal / reciprocal square root: MUFU seed, one third-order correction, one Newton
+// step (~1 ulp, UNBIASED). The MUFU f64 seeds are coarse (~2^-14 relative); two plain Newton
+// steps from them leave a systematic -1.5 e1^2 error (Newton for rsqrt / rcp converges from
+// below) of ~0.2 ulp, which the Jacobi rotations turned into a steady shrink of the V columns
+// (mean ||v_j||^2 - 1 of -1.9e-15 vs the oracle's +2.6e-16 at 64 x 64, growing linearly through
+// the block method's V_R products). The cubic first step leaves e1 ~ e0^3, so the final Newton
+// step's quadratic term is far below an ulp and only round-to-nearest errors remain.
 // Only used on arguments in the normal range (callers fall back otherwise).
 BF_DEV double rcp_fast(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
   double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
+  r = fma(r, fma(e, e, e), r);  // r (1 + e + e^2): error O(e^3)
   e = fma(-x, r, 1.0);
   return fma(r, e, r);
 }
@@ -45,12 +51,12 @@ BF_DEV double rcp_fast(double x) {
 BF_DEV double rsqrt_fast(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  // y <- y * (1.5 - 0.5 x y^2), twice
-  double hx = 0.5 * x;
-  double t = fma(-hx * y, y, 0.5);
-  y = fma(y, t, y);
-  t = fma(-hx * y, y, 0.5);
-  return fma(y, t, y);
+  // e = 1 - x y^2; y (1 + e/2 + 3 e^2 / 8) has error O(e^3)
+  double e = fma(-x * y, y, 1.0);
+  y = fma(y * e, fma(e, 0.375, 0.5), y);
+  // Newton: y (1 + e/2)
+  e = fma(-x * y, y, 1.0);
+  return fma(y * 0.5, e, y);
 }
 
 // householder_vector's scalars (qr.py:26-48) on the fast reciprocal paths:
@@ -80,6 +86,19 @@ BF_DEV double div_by(double x, double d, double r) {
   return fma(fma(-q, d, x), r, q);
 }
 
+// Norm-preserving cosine: given c0 ~ 1/sqrt(1 + t^2) (within a few ulp) and the tangent t that
+// the caller applies (s = c t), return c with c^2 (1 + t^2) = 1 to second order: the residual
+// rho = 1 - c0^2 - (c0 t)^2 is formed with FMAs (exact products) and c = c0 (1 + rho / 2).
+// Without it, c = dd / hypot(dd, den) rounds independently of t and the rotations shrank the V
+// columns on average (mean ||v_j||^2 - 1 of -1.9e-15 at 64 x 64 vs the reference's +1.7e-16;
+// x56 V_R products in the block method). With it the drift is gone and ||V^T V - I|| falls below
+// the reference's (whose c = 1 / hypot(1, t) is exactly 1 for |t| < 1e-8, an expansion).
+BF_DEV double unit_cos(double c0, double t) {
+  const double s0 = c0 * t;
+  const double rho = fma(-s0, s0, fma(-c0, c0, 1.0));
+  return fma(c0 * 0.5, rho, c0);
+}
+
 // Rutishauser rotation returning t as well (jacobi.py:68-80), g_pq != 0:
 //   zeta = (g_qq - g_pp) / (2 g_pq), t = sign(zeta) / (|zeta| + hypot(1, zeta)),
 //   c = 1 / hypot(1, t), s = c t.
@@ -89,6 +108,15 @@ BF_DEV double div_by(double x, double d, double r) {
 // multiplied through by |den|, which leaves two independent reciprocal chains (t and c, s)
 // after h instead of four dependent ones. Exact IEEE fallback outside [1e-150, 1e150].
 BF_DEV void jacobi_rotation_t(double gpp, double gpq, double gqq, double& c, double& s, double& t) {
+#if defined(BF_EXP_ROT) && BF_EXP_ROT == 1
+  {  // experiment: the reference's formula with IEEE division / sqrt
+    const double zeta = (gqq - gpp) / (2.0 * gpq);
+    t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+    c = 1.0 / sqrt(fma(t, t, 1.0));
+    s = c * t;
+    return;
+  }
+#endif
   const double den = 2.0 * gpq, diff = gqq - gpp;
   const double aden = fabs(den), adiff = fabs(diff);
   const double big = aden > adiff ? aden : adiff;
@@ -103,8 +131,8 @@ BF_DEV void jacobi_rotation_t(double gpp, double gpq, double gqq, double& c, dou
     const double q2 = fma(dd, dd, den * den);
     const double r2 = rsqrt_fast(q2);  // 1 / hypot(dd, den)
     t = sden * rcp_fast(dd);
-    c = dd * r2;
-    s = sden * r2;
+    c = unit_cos(dd * r2, t);
+    s = c * t;
   } else {
     const double zeta = diff / den;
     t = copysign(1.0, zeta) / (fabs(zeta) + hypot(1.0, zeta));
@@ -133,7 +161,7 @@ BF_DEV void jacobi_rotation(double gpp, double gpq, double gqq, double& c, doubl
     } else {
       t = copysign(0.5 / az, zeta);  // az + hypot(1, az) == 2 az in double
     }
-    c = rsqrt_fast(fma(t, t, 1.0));
+    c = unit_cos(rsqrt_fast(fma(t, t, 1.0)), t);
     s = c * t;
   } else {
     double zeta = diff / den;

@@ -37,14 +37,21 @@ def svd_variants(name, a, threads=16):
     a3 = np.ascontiguousarray(a_np.transpose(0, 2, 1))
     o = orc.batch_svd_stacked(a3, m, n, ordering="round_robin", accumulate_v=True, threads=threads)
     u_o, s_o, v_o = o["u"].transpose(0, 2, 1), o["s"], o["v"].transpose(0, 2, 1)
+    def nbias(v):  # mean and std of ||v_j||^2 - 1 over all columns: a systematic drift shows as mean != 0
+        d = np.sum(np.asarray(v, np.float64) ** 2, axis=1) - 1.0
+        return [float(d.mean()), float(d.std())]
+
     out = {"oracle": {"orth_u": d3(orth_res(u_o)), "orth_v": d3(orth_res(v_o)),
-                      "recon": d3(recon_res(a_np, u_o, s_o, v_o))}}
+                      "recon": d3(recon_res(a_np, u_o, s_o, v_o)), "vnorm_bias": nbias(v_o),
+                      "rotations": float(o["rotations"].mean()), "sweeps": float(o["sweeps"].mean())}}
     for tier in ("auto", "shared"):
-        r = bf.svd_tensor(a, bf.JacobiOptions(ordering="round_robin", accumulate_v=True, tier=tier))
+        r = bf.svd_tensor(a, bf.JacobiOptions(ordering="round_robin", accumulate_v=True, tier=tier), rotations=True)
         u, s, v = np3(r["u"]), np3(r["sigma"]), np3(r["v"])
+        rot = float(np3(r["rotations"]).mean()) if r["rotations"] is not None else -1.0
         nw, _ = sigma_stats(s, s_o)
         out[tier] = {"orth_u": d3(orth_res(u)), "orth_v": d3(orth_res(v)), "recon": d3(recon_res(a_np, u, s, v)),
-                     "sigma_normwise": d3(nw)}
+                     "sigma_normwise": d3(nw), "vnorm_bias": nbias(v), "rotations": rot,
+                     "sweeps": float(np3(r["sweeps"]).mean())}
     print(json.dumps({name: out}), flush=True)
 
 
@@ -69,6 +76,13 @@ def block_partial(name, a, sweeps, threads=16):
 
 def main():
     orc.build()
+    if len(sys.argv) > 1 and sys.argv[1] == "quick":
+        p = bf.gaussian_tensor(500, 256, 64, 4_000_000, seed_mode="add")
+        _, r = bf.qr_tensor(p)
+        svd_variants("R64_upper", r.contiguous())
+        svd_variants("gauss32", bf.gaussian_tensor(500, 32, 32, 1_000_000, seed_mode="add"))
+        block_partial("cfg4d_40", bf.gaussian_tensor(40, 256, 256, 4_000_000, seed_mode="add"), [30])
+        return
     torch.manual_seed(0)
     a = bf.gaussian_tensor(500, 64, 64, 3_000_000, seed_mode="add")
     svd_variants("gauss64", a)
