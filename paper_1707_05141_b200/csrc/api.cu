@@ -137,7 +137,6 @@ int block_impl(int64_t batch, int m, int n, const T* a, T* u, T* s, T* v, int32_
   if (!sweeps || !conv) return fail(BF_ERR_ARG, "sweeps and converged are required for block_svd");
   int k = o->block_width;
   if (o->method == 1) k = std::max(1, std::min(k, m / 2));
-  if (2 * k > 64) return fail(BF_ERR_UNSUPPORTED, "block_width %d unsupported (2*block_width must be <= 64)", k);
   if (m == 0) return fail(BF_ERR_UNSUPPORTED, "block_svd of an empty matrix is unsupported");
   const bool f64 = sizeof(T) == 8;
   int dt = f64 ? 0 : 1;

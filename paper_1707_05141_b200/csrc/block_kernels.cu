@@ -752,6 +752,100 @@ __global__ void __launch_bounds__(256) bj_extract(BJArgs<T> a, T* U, T* S, T* Vo
                      sig, order, cand_g + b * 2 * (int64_t)m, flag);
 }
 
+// ---- wide block pairs (2k > 64, any block_width: blockjacobi.py:98-104 accepts every width).
+// The pair is staged into a contiguous per-slot copy and the step runs as batched launches over
+// all slots of the step: gather -> (Gram: G = P^T P | direct: P = Q R) -> e = scaled_offdiag
+// (pairs at e <= tol skipped, blockjacobi.py:128-129,139-140) -> inner round-robin SVD (batched,
+// masked by the pair flags) -> P U (Gram, null directions zeroed, :132-134) or (Q U_R) sigma
+// (direct, :143) and the V pair times the rotation (:146-149) -> scatter of the active pairs.
+template <typename T>
+struct BWArgs {
+  T *P, *PV, *G, *Q, *U, *S, *VR, *Pn, *PVn;
+  uint8_t* pact;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) bw_gather(BJArgs<T> a, BWArgs<T> w, int step) {
+  const int P = a.nb / 2;
+  const int64_t slot = blockIdx.x, b = slot / P;
+  if (b >= a.batch) return;
+  if (!a.active[b]) {
+    if (threadIdx.x == 0) w.pact[slot] = 0;
+    return;
+  }
+  int bi, bj;
+  rr_pair(a.nb, step, (int)(slot % P), bi, bj);
+  const int k = a.k, kk = 2 * k, m = a.m, np = a.n_pad;
+  const T* Wb = a.W + b * (int64_t)m * np;
+  T* Ps = w.P + slot * (int64_t)m * kk;
+  for (int64_t e = threadIdx.x; e < (int64_t)m * kk; e += blockDim.x) {
+    const int c = (int)(e / m), r = (int)(e % m);
+    Ps[e] = Wb[(int64_t)pair_col(c, k, bi, bj) * m + r];
+  }
+  if (a.V) {
+    const T* Vb = a.V + b * (int64_t)np * np;
+    T* Vs = w.PV + slot * (int64_t)np * kk;
+    for (int64_t e = threadIdx.x; e < (int64_t)np * kk; e += blockDim.x) {
+      const int c = (int)(e / np), r = (int)(e % np);
+      Vs[e] = Vb[(int64_t)pair_col(c, k, bi, bj) * np + r];
+    }
+  }
+}
+
+// e = scaled_offdiag of G (Gram: mirrored upper triangle first, syrk core.py:68-78) or R (direct)
+template <typename T>
+__global__ void __launch_bounds__(256) bw_offdiag(BJArgs<T> a, BWArgs<T> w, int gram) {
+  __shared__ double red;
+  const int P = a.nb / 2;
+  const int64_t slot = blockIdx.x, b = slot / P;
+  if (b >= a.batch || !a.active[b]) return;
+  const int kk = 2 * a.k;
+  T* M = w.G + slot * (int64_t)kk * kk;
+  if (gram) {
+    for (int e = threadIdx.x; e < kk * kk; e += blockDim.x) {
+      const int j = e / kk, i = e % kk;  // row i, column j
+      if (i > j) M[(size_t)j * kk + i] = M[(size_t)i * kk + j];
+    }
+    __syncthreads();
+  }
+  const double e = scaled_offdiag_cta<T>(M, kk, kk, &red);
+  if (threadIdx.x == 0) {
+    atomic_max_pos(a.e_sweep + b, e);
+    w.pact[slot] = e > a.tol ? 1 : 0;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) bw_scatter(BJArgs<T> a, BWArgs<T> w, int step, int gram) {
+  const int P = a.nb / 2;
+  const int64_t slot = blockIdx.x, b = slot / P;
+  if (b >= a.batch || !w.pact[slot]) return;
+  int bi, bj;
+  rr_pair(a.nb, step, (int)(slot % P), bi, bj);
+  const int k = a.k, kk = 2 * k, m = a.m, np = a.n_pad;
+  T* Wb = a.W + b * (int64_t)m * np;
+  const T* Pn = w.Pn + slot * (int64_t)m * kk;
+  const T* S = w.S + slot * (int64_t)kk;
+  for (int64_t e = threadIdx.x; e < (int64_t)m * kk; e += blockDim.x) {
+    const int c = (int)(e / m), r = (int)(e % m);
+    const T sg = S[c];
+    T x = Pn[e];
+    if (gram)
+      x = sg != T(0) ? x : T(0);  // exactly-null directions stay null (blockjacobi.py:133-134)
+    else
+      x = x * sg;  // (Q @ U_R) * sigma (blockjacobi.py:143)
+    Wb[(int64_t)pair_col(c, k, bi, bj) * m + r] = x;
+  }
+  if (a.V) {
+    T* Vb = a.V + b * (int64_t)np * np;
+    const T* Vs = w.PVn + slot * (int64_t)np * kk;
+    for (int64_t e = threadIdx.x; e < (int64_t)np * kk; e += blockDim.x) {
+      const int c = (int)(e / np), r = (int)(e % np);
+      Vb[(int64_t)pair_col(c, k, bi, bj) * np + r] = Vs[e];
+    }
+  }
+}
+
 static void bj_geometry(int m, int n, int bw, int method, int& k, int& n_pad, int& nb) {
   k = bw;
   if (method == 1) {
@@ -773,7 +867,12 @@ static size_t direct_smem(int m, int kk, bool p_in) {
 template <typename T>
 struct BJLayout {
   size_t w, v, p, e, act, cand, g, u, s, pact, iws, dp, dtau, dvr, total;
+  // wide pairs (2k > 64)
+  size_t xp, xpv, xq, xvr, xpn, xpvn, xqws;
 };
+
+// 2k > 64: the staged wide-pair pipeline (any block width)
+static bool bj_wide(int kk) { return kk > 64; }
 
 // batched direct pipeline: fp64, 2k in {16, 32, 48, 64} (register-tier inner SVD with V), the
 // pair plus the reflector stage fitting one CTA's shared memory
@@ -824,8 +923,36 @@ static BJLayout<T> bj_layout(int64_t batch, int m, int n, int bw, int method, bo
   off += bd ? al((size_t)slots * kk * sizeof(T)) : 0;
   L.dvr = off;
   off += bd ? al((size_t)slots * kk * kk * sizeof(T)) : 0;
+  const bool wide = bj_wide(kk);
+  const size_t es = sizeof(T);
+  if (wide) {  // G doubles as R (direct); U, S, pact as above
+    L.g = off;
+    off += al((size_t)slots * kk * kk * es);
+    L.u = off;
+    off += al((size_t)slots * kk * kk * es);
+    L.s = off;
+    off += al((size_t)slots * kk * es);
+    L.pact = off;
+    off += al((size_t)slots);
+    L.xp = off;
+    off += al((size_t)slots * m * kk * es);
+    L.xpn = off;
+    off += al((size_t)slots * m * kk * es);
+    L.xq = off;
+    off += method == 1 ? al((size_t)slots * m * kk * es) : 0;
+    L.xpv = off;
+    off += accv ? al((size_t)slots * np * kk * es) : 0;
+    L.xpvn = off;
+    off += accv ? al((size_t)slots * np * kk * es) : 0;
+    L.xvr = off;
+    off += (method == 1 && accv) ? al((size_t)slots * kk * kk * es) : 0;
+    L.xqws = off;
+    off += method == 1 ? al(qr_global_ws_bytes(es == 8 ? 0 : 1, slots, m, kk)) : 0;
+  }
   L.iws = off;
-  off += bt ? al(svd_global_ws_bytes(sizeof(T) == 8 ? 0 : 1, slots, kk, kk, 1, bd, 0, 30)) : 0;
+  off += (bt || wide) ? al(svd_global_ws_bytes(es == 8 ? 0 : 1, slots, kk, kk, 1, bd || (wide && method == 1 && accv),
+                                               0, 30))
+                      : 0;
   L.total = off;
   return L;
 }
@@ -871,15 +998,17 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
   bj_init<T><<<(unsigned)L.batch, 256, 0, st>>>(a, (const T*)L.a);
   if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
   const unsigned grid = (unsigned)(L.batch * (nb / 2));
-  size_t smem;
-  if (L.method == 0) {
-    smem = (size_t)(2 * kk * kk + kk * 32 + 3 * kk) * sizeof(T) + (size_t)kk * sizeof(int) + 64;
-    e = cudaFuncSetAttribute(bj_gram_step<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  } else {
-    smem = direct_smem<T>(L.m, kk, a.p_in_smem);
-    e = cudaFuncSetAttribute(bj_direct_step<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  size_t smem = 0;
+  if (!bj_wide(kk)) {  // the one-CTA-per-pair step kernels (the wide pipeline needs no large smem)
+    if (L.method == 0) {
+      smem = (size_t)(2 * kk * kk + kk * 32 + 3 * kk) * sizeof(T) + (size_t)kk * sizeof(int) + 64;
+      e = cudaFuncSetAttribute(bj_gram_step<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    } else {
+      smem = direct_smem<T>(L.m, kk, a.p_in_smem);
+      e = cudaFuncSetAttribute(bj_direct_step<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    if (e != cudaSuccess) return (int)e;
   }
-  if (e != cudaSuccess) return (int)e;
   const bool bg = bj_batched_gram(L.method, kk);
   BJGemmArgs<T> g;
   // TMA staging of the DMMA block kernels (bit 0 Gram, bit 1 rotation); BF_BLOCK_TMA overrides
@@ -994,11 +1123,74 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(bj_rot_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRotSmem);
     if (e != cudaSuccess) return (int)e;
   }
+  // wide pairs (2k > 64): staged pipeline over batched QR / GEMM / SVD launches
+  const bool wide = bj_wide(kk);
+  BWArgs<T> wa{};
+  SvdLaunch win{};
+  if (wide) {
+    wa.P = (T*)(base + lay.xp);
+    wa.Pn = (T*)(base + lay.xpn);
+    wa.Q = L.method == 1 ? (T*)(base + lay.xq) : nullptr;
+    wa.PV = L.v ? (T*)(base + lay.xpv) : nullptr;
+    wa.PVn = L.v ? (T*)(base + lay.xpvn) : nullptr;
+    wa.VR = (L.method == 1 && L.v) ? (T*)(base + lay.xvr) : nullptr;
+    wa.G = (T*)(base + lay.g);
+    wa.U = (T*)(base + lay.u);
+    wa.S = (T*)(base + lay.s);
+    wa.pact = (uint8_t*)(base + lay.pact);
+    // inner SVD (blockjacobi.py:79-81): round robin, default tolerance; V only for the direct
+    // method's rotation (:141, :145)
+    win.batch = L.batch * (nb / 2);
+    win.m = kk;
+    win.n = kk;
+    win.a = wa.G;
+    win.a_stride = (int64_t)kk * kk;
+    win.u = wa.U;
+    win.u_stride = (int64_t)kk * kk;
+    win.s = wa.S;
+    win.s_stride = kk;
+    win.v = wa.VR;
+    win.v_stride = (int64_t)kk * kk;
+    win.sweeps = nullptr;
+    win.converged = nullptr;
+    win.rotations = nullptr;
+    win.tol = a.tol_inner;
+    win.max_sweeps = 30;
+    win.ordering = 1;
+    win.tier = 0;
+    win.transpose_a = false;
+    win.active = wa.pact;
+  }
   void* iws = base + lay.iws;
   const size_t iws_bytes = lay.total - lay.iws;
   for (int sw = 0; sw < L.max_sweeps; ++sw) {
     for (int s = 0; s < nb - 1; ++s) {
-      if (bd) {
+      if (wide) {
+        const int dt = sizeof(T) == 8 ? 0 : 1;
+        const int64_t slots = L.batch * (nb / 2);
+        const int64_t mk = (int64_t)L.m * kk, k2 = (int64_t)kk * kk, vk = (int64_t)np * kk;
+        bw_gather<T><<<grid, 256, 0, st>>>(a, wa, s);
+        int rc;
+        GemmLaunch gl;
+        if (L.method == 0) {  // G = P^T P (upper triangle mirrored in bw_offdiag)
+          gl = GemmLaunch{slots, kk, kk, L.m, wa.P, L.m, mk, true, wa.P, L.m, mk, false, wa.G, kk, k2};
+          if ((rc = launch_gemm(dt, gl, st))) return rc;
+        } else {  // (Q, R) = qr(P)
+          if ((rc = launch_qr(dt, slots, L.m, kk, wa.P, mk, wa.Q, mk, wa.G, k2, base + lay.xqws, st))) return rc;
+        }
+        bw_offdiag<T><<<grid, 256, 0, st>>>(a, wa, L.method == 0);
+        if ((rc = launch_svd(dt, win, iws, iws_bytes, st))) return rc;
+        // Gram: P U_G; direct: Q U_R (sigma applied in the scatter)
+        gl = GemmLaunch{slots, L.m, kk, kk, L.method == 0 ? wa.P : wa.Q, L.m, mk, false, wa.U, kk, k2, false,
+                        wa.Pn, L.m, mk};
+        if ((rc = launch_gemm(dt, gl, st))) return rc;
+        if (L.v) {  // V pair @ rot (rot = U_G | V_R)
+          gl = GemmLaunch{slots, np, kk, kk, wa.PV, np, vk, false, L.method == 0 ? wa.U : wa.VR, kk, k2, false,
+                          wa.PVn, np, vk};
+          if ((rc = launch_gemm(dt, gl, st))) return rc;
+        }
+        bw_scatter<T><<<grid, 256, 0, st>>>(a, wa, s, L.method == 0);
+      } else if (bd) {
         if (dqr_reg)
           bj_dqr_reg<<<grid, 256, dqr_smem, st>>>(*reinterpret_cast<BJArgs<double>*>(&a), dd, s);
         else

@@ -152,8 +152,14 @@ def test_svd_golden(nm, tier):
         assert vec_mismatch(r.v, c["v"], c["sigma"], a.dtype) <= 1.0
         if a.size and c["sigma"][0] > 0:
             assert recon_residual(a, r.u, r.sigma, r.v) <= 64 * np.finfo(a.dtype).eps * a.shape[1]
-    if a.shape[1] and a.dtype == np.float64:
-        assert orth_residual(r.u) <= max(10 * orth_residual(c["u"]), 1e-13)
+    if a.shape[1] and a.dtype == np.float64 and c["sigma"].size and c["sigma"][0] > 0:
+        # residuals no worse than the reference's own on the same matrix (north star). U's
+        # orthogonality is set by the convergence tolerance, not rounding: equal to ~1 %.
+        eps_n = np.finfo(np.float64).eps * a.shape[1]
+        assert orth_residual(r.u) <= 1.02 * orth_residual(c["u"]) + eps_n
+        if bool(c["accumulate_v"]):
+            assert orth_residual(r.v) <= orth_residual(c["v"]) + eps_n
+            assert recon_residual(a, r.u, r.sigma, r.v) <= recon_residual(a, c["u"], c["sigma"], c["v"]) + eps_n
 
 
 @pytest.mark.parametrize("ordering", ["serial", "round_robin"])
@@ -216,17 +222,30 @@ def test_svd_f32_shared_tier_vs_oracle(ordering):
     assert float(((ad - rec).norm(dim=(1, 2)) / ad.norm(dim=(1, 2))).max()) < 1e-5
 
 
-def test_svd_cfg1_full_batch_properties():
+@pytest.mark.parametrize("ordering", ["serial", "round_robin"])
+def test_svd_cfg1_full_batch_properties(ordering):
+    """All 1,000 cfg1 matrices: the residual maxima are no worse than the oracle's own maxima on
+    the same batch, and below SURVEY §8c's bars (7.0e-14 / 1.6e-14 / 2.9e-15)."""
     a = dev_gauss(1000, 32, 32, 1_000_000)
-    r = bf.svd_tensor(a, bf.JacobiOptions(ordering="serial", accumulate_v=True))
+    r = bf.svd_tensor(a, bf.JacobiOptions(ordering=ordering, accumulate_v=True))
     u, s, v = r["u"], r["sigma"], r["v"]
     eye = torch.eye(32, dtype=torch.float64, device=a.device)
     assert torch.all(r["converged"])
-    assert float((u.transpose(1, 2) @ u - eye).norm(dim=(1, 2)).max()) < 1e-13
-    assert float((v.transpose(1, 2) @ v - eye).norm(dim=(1, 2)).max()) < 1e-13
+    o = orc.batch_svd_stacked(stack_np(a), 32, 32, ordering=ordering, accumulate_v=True, threads=8)
+    ao = torch.as_tensor(stack_np(a)).transpose(1, 2)
+    uo, vo = torch.as_tensor(o["u"]).transpose(1, 2), torch.as_tensor(o["v"]).transpose(1, 2)
+    so = torch.as_tensor(o["s"])
+    e = torch.eye(32, dtype=torch.float64)
+    ou_o = float((uo.transpose(1, 2) @ uo - e).norm(dim=(1, 2)).max())
+    ov_o = float((vo.transpose(1, 2) @ vo - e).norm(dim=(1, 2)).max())
+    rc_o = float(((ao - (uo * so[:, None, :]) @ vo.transpose(1, 2)).norm(dim=(1, 2)) / ao.norm(dim=(1, 2))).max())
+    ou = float((u.transpose(1, 2) @ u - eye).norm(dim=(1, 2)).max())
+    ov = float((v.transpose(1, 2) @ v - eye).norm(dim=(1, 2)).max())
     rec = (u * s[:, None, :]) @ v.transpose(1, 2)
-    rel = (a - rec).norm(dim=(1, 2)) / a.norm(dim=(1, 2))
-    assert float(rel.max()) < 1e-14
+    rc = float(((a - rec).norm(dim=(1, 2)) / a.norm(dim=(1, 2))).max())
+    assert ou <= ou_o and ou <= 7.1e-14, (ou, ou_o)
+    assert ov <= ov_o and ov <= 1.6e-14, (ov, ov_o)
+    assert rc <= rc_o and rc <= 2.9e-15, (rc, rc_o)
     assert bool(torch.all(s[:, :-1] >= s[:, 1:]))
 
 
@@ -323,6 +342,47 @@ def test_block_cfg4_gram_vs_oracle():
     rec = (u * r["sigma"][:, None, :]) @ v.transpose(1, 2)
     rel = (a - rec).norm(dim=(1, 2)) / a.norm(dim=(1, 2))
     assert float(rel.max()) < 1e-12
+
+
+@pytest.mark.parametrize("method", ["gram", "direct"])
+@pytest.mark.parametrize("m,n,bw,dtype", [(256, 256, 64, np.float64), (200, 150, 48, np.float64),
+                                          (160, 120, 40, np.float32), (130, 130, 100, np.float64)])
+def test_block_wide_width_vs_oracle(method, m, n, bw, dtype):
+    """block_width > 32 (pair width 2k > 64; the reference accepts any width, blockjacobi.py:98-104):
+    the staged wide-pair pipeline against the oracle -- sigma, vectors, flags, sweeps, e_history."""
+    B = 3
+    a = dev_gauss(B, m, n, 4_200_000 + m + n + bw)
+    if dtype == np.float32:
+        a = a.float()
+    tol = 1e-11 if method == "gram" and dtype == np.float64 else None
+    opts = bf.BlockJacobiOptions(method=method, block_width=bw, tolerance=tol, accumulate_v=True)
+    r = bf.block_svd_tensor(a, opts)
+    otol = tol if tol is not None else (1e-13 if dtype == np.float64 else 1e-5)
+    o = orc.batch_block_svd_stacked(stack_np(a), m, n, block_width=bw, method=method, tol=otol,
+                                    accumulate_v=True, threads=B)
+    s = r["sigma"].cpu().numpy()
+    sw = r["sweeps"].cpu().numpy()
+    cv = r["converged"].cpu().numpy()
+    eh = r["e_history"].cpu().numpy()
+    u, v = stack_np(r["u"]), stack_np(r["v"])
+    for b in range(B):
+        assert sigma_normwise(s[b], o["s"][b]) <= gate(dtype)
+        so = int(o["sweeps"][b])
+        eo = o["e_history"][b, :so]
+        k = min(so, int(sw[b]))
+        big = eo[:k] > (1e-8 if dtype == np.float64 else 1e-3)
+        assert np.allclose(eh[b, :k][big], eo[:k][big], rtol=1e-3 if dtype == np.float64 else 1e-2)
+        decisive = so < 2 or (eo[-1] < otol and eo[-2] > 3 * otol)
+        if decisive:
+            assert abs(int(sw[b]) - so) <= 1
+            assert bool(cv[b]) == bool(o["converged"][b])
+        if dtype == np.float64 and bool(o["converged"][b]):
+            assert vec_mismatch(u[b].T, o["u"][b].T, o["s"][b], np.float64, factor=4096.0) <= 1.0
+            assert vec_mismatch(v[b].T, o["v"][b].T, o["s"][b], np.float64, factor=4096.0) <= 1.0
+    ad = a.double()
+    rec = (r["u"].double() * r["sigma"].double()[:, None, :]) @ r["v"].double().transpose(1, 2)
+    rel = (ad - rec).norm(dim=(1, 2)) / ad.norm(dim=(1, 2))
+    assert float(rel.max()) < (1e-12 if dtype == np.float64 else 1e-4)
 
 
 @pytest.mark.parametrize("m,n", [(256, 256), (200, 128), (300, 128)])

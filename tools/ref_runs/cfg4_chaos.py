@@ -12,7 +12,9 @@ import multiprocessing as mp
 import os
 import sys
 
-import numpy as np
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+
+import numpy as np  # noqa: E402
 
 REF = "/root/reference/pkg/src"
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -38,7 +40,7 @@ def main():
     rng = np.random.default_rng(0)
     others = sorted(set(rng.choice(1000, 60, replace=False).tolist()) - set(outl))[:40]
     idx = sorted(set(outl) | set(others))
-    with mp.Pool(len(os.sched_getaffinity(0))) as pool:
+    with mp.get_context("spawn").Pool(len(os.sched_getaffinity(0))) as pool:
         ref = pool.map(ref_entry, idx)
     out = []
     for i, sw, cv, eh in ref:
