@@ -93,6 +93,16 @@ BF_API int bf_block_svd_batched_f64(int64_t batch, int32_t m, int32_t n, const d
 BF_API int bf_block_svd_batched_f32(int64_t batch, int32_t m, int32_t n, const float* a, float* u, float* sigma,
                              float* v, int32_t* sweeps, uint8_t* converged, float* e_history,
                              const bf_block_opts* opts, void* workspace, size_t workspace_bytes, void* stream);
+/* Same, plus per-matrix work counters (stats: batch x 4 int64, nullable): [0] pair visits (Gram or
+ * pair QR + e = scaled_offdiag), [1] rotated pairs (e > tol), [2] inner-SVD pair visits (inner
+ * sweeps x 2k(2k-1)/2), [3] inner-SVD rotations -- the run's own counts behind the algorithmic
+ * flop figure (no reference counterpart; measurement extension). */
+BF_API int bf_block_svd_batched_ex_f64(int64_t batch, int32_t m, int32_t n, const double* a, double* u, double* sigma,
+                                double* v, int32_t* sweeps, uint8_t* converged, double* e_history, int64_t* stats,
+                                const bf_block_opts* opts, void* workspace, size_t workspace_bytes, void* stream);
+BF_API int bf_block_svd_batched_ex_f32(int64_t batch, int32_t m, int32_t n, const float* a, float* u, float* sigma,
+                                float* v, int32_t* sweeps, uint8_t* converged, float* e_history, int64_t* stats,
+                                const bf_block_opts* opts, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- batched randomized SVD (Alg. 4): entry b uses seed ^ (index_base + b) (rsvd.py:79-86),
  * seed = seed_lo | seed_hi << 64. omega (nullable): batch x (n x (k+p)) sketch supplied by the

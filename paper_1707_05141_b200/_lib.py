@@ -61,6 +61,8 @@ EXPORTS = (
     "bf_block_svd_workspace_size",
     "bf_block_svd_batched_f64",
     "bf_block_svd_batched_f32",
+    "bf_block_svd_batched_ex_f64",
+    "bf_block_svd_batched_ex_f32",
     "bf_rsvd_workspace_size",
     "bf_rsvd_batched_f64",
     "bf_rsvd_batched_f32",
@@ -114,6 +116,10 @@ def load():
     for name in ("bf_block_svd_batched_f64", "bf_block_svd_batched_f32"):
         f = getattr(L, name)
         f.argtypes = [I64, I32, I32, P, P, P, P, P, P, P, ctypes.POINTER(_BlockOpts), P, SZ, P]
+        f.restype = ctypes.c_int
+    for name in ("bf_block_svd_batched_ex_f64", "bf_block_svd_batched_ex_f32"):
+        f = getattr(L, name)
+        f.argtypes = [I64, I32, I32, P, P, P, P, P, P, P, P, ctypes.POINTER(_BlockOpts), P, SZ, P]
         f.restype = ctypes.c_int
     L.bf_rsvd_workspace_size.argtypes = [I64, I32, I32, I32, I32, I32]
     L.bf_rsvd_workspace_size.restype = SZ

@@ -81,7 +81,9 @@ def _validate(a):
         raise ValueError(f"block_svd requires m >= n, got {m} x {n}")
 
 
-def block_svd_colmajor(store, m, n, opts):
+def block_svd_colmajor(store, m, n, opts, *, stats=False):
+    """One C-ABI call on column-major storage (B, n, m). stats=True also returns the per-matrix
+    work counters (B, 4): pair visits, rotated pairs, inner-SVD pair visits, inner rotations."""
     L = _lib.load()
     dev = store.device
     B = store.shape[0]
@@ -95,21 +97,23 @@ def block_svd_colmajor(store, m, n, opts):
     sweeps = torch.empty(B, dtype=torch.int32, device=dev)
     conv = torch.empty(B, dtype=torch.uint8, device=dev)
     ws, wsb = workspace(L.bf_block_svd_workspace_size(B, m, n, es, copts), dev)
-    fn = L.bf_block_svd_batched_f64 if es == 8 else L.bf_block_svd_batched_f32
+    st = torch.zeros((B, 4), dtype=torch.int64, device=dev) if stats else None
+    fn = L.bf_block_svd_batched_ex_f64 if es == 8 else L.bf_block_svd_batched_ex_f32
     with torch.cuda.device(dev):
-        rc = fn(B, m, n, ptr(store), ptr(u), ptr(s), ptr(v), ptr(sweeps), ptr(conv), ptr(eh), copts, ptr(ws), wsb,
-                stream_handle(dev))
+        rc = fn(B, m, n, ptr(store), ptr(u), ptr(s), ptr(v), ptr(sweeps), ptr(conv), ptr(eh), ptr(st), copts,
+                ptr(ws), wsb, stream_handle(dev))
     _lib.check(rc, "block_svd")
-    return dict(u=u, s=s, v=v, sweeps=sweeps, converged=conv, e_history=eh)
+    return dict(u=u, s=s, v=v, sweeps=sweeps, converged=conv, e_history=eh, stats=st)
 
 
-def block_svd_tensor(a, opts=None):
-    """Tensor-native batched block Jacobi SVD of a (B, m, n) CUDA tensor."""
+def block_svd_tensor(a, opts=None, *, stats=False):
+    """Tensor-native batched block Jacobi SVD of a (B, m, n) CUDA tensor (stats: see
+    :func:`block_svd_colmajor`)."""
     opts = opts or BlockJacobiOptions()
     check_batched_tensor(a, "block_svd_tensor")
     B, m, n = a.shape
     _validate(np.empty((m, n)))
-    r = block_svd_colmajor(colmajor(a), m, n, opts)
+    r = block_svd_colmajor(colmajor(a), m, n, opts, stats=stats)
     return dict(
         u=from_colmajor(r["u"]),
         sigma=r["s"],
@@ -117,6 +121,7 @@ def block_svd_tensor(a, opts=None):
         sweeps=r["sweeps"],
         converged=r["converged"].bool(),
         e_history=r["e_history"],
+        stats=r["stats"],
     )
 
 

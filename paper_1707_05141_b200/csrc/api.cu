@@ -127,7 +127,7 @@ int check_bopts(const bf_block_opts* o) {
 
 template <typename T>
 int block_impl(int64_t batch, int m, int n, const T* a, T* u, T* s, T* v, int32_t* sweeps, uint8_t* conv, T* eh,
-               const bf_block_opts* o, void* ws, size_t wsb, void* st) {
+               const bf_block_opts* o, void* ws, size_t wsb, void* st, int64_t* stats = nullptr) {
   int rc = check_bopts(o);
   if (rc) return rc;
   if (batch < 0 || m < 0 || n < 0) return fail(BF_ERR_ARG, "negative batch or shape");
@@ -157,6 +157,7 @@ int block_impl(int64_t batch, int m, int n, const T* a, T* u, T* s, T* v, int32_
   L.method = o->method;
   L.max_sweeps = o->max_sweeps;
   L.tol = resolve_tol(o->tolerance, f64, true);
+  L.stats = stats;
   return cuda_rc(bf::launch_block_svd(dt, L, ws, S(st)), "block_svd");
 }
 
@@ -351,6 +352,16 @@ int bf_block_svd_batched_f32(int64_t batch, int32_t m, int32_t n, const float* a
                              int32_t* sweeps, uint8_t* conv, float* eh, const bf_block_opts* o, void* ws, size_t wsb,
                              void* st) {
   return block_impl<float>(batch, m, n, a, u, s, v, sweeps, conv, eh, o, ws, wsb, st);
+}
+int bf_block_svd_batched_ex_f64(int64_t batch, int32_t m, int32_t n, const double* a, double* u, double* s, double* v,
+                                int32_t* sweeps, uint8_t* conv, double* eh, int64_t* stats, const bf_block_opts* o,
+                                void* ws, size_t wsb, void* st) {
+  return block_impl<double>(batch, m, n, a, u, s, v, sweeps, conv, eh, o, ws, wsb, st, stats);
+}
+int bf_block_svd_batched_ex_f32(int64_t batch, int32_t m, int32_t n, const float* a, float* u, float* s, float* v,
+                                int32_t* sweeps, uint8_t* conv, float* eh, int64_t* stats, const bf_block_opts* o,
+                                void* ws, size_t wsb, void* st) {
+  return block_impl<float>(batch, m, n, a, u, s, v, sweeps, conv, eh, o, ws, wsb, st, stats);
 }
 
 size_t bf_rsvd_workspace_size(int64_t batch, int32_t m, int32_t n, int32_t k, int32_t p, int32_t es) {

@@ -26,10 +26,18 @@ struct BJGemmArgs {
   double* e_sweep;
   double tol;
   int only_v = 0;
+  int64_t* stats = nullptr;  // batch x 4 work counters (BlockLaunch::stats) or null
   int tma = 3;  // bit 0: bj_gram_mma, bit 1: bj_rot_mma stage with TMA bulk copies (even ld)  // bj_rot_mma: update the V pair only (direct method)
 };
 
 BF_DEV int bj_pair_col(int c, int k, int bi, int bj) { return c < k ? bi * k + c : bj * k + (c - k); }
+
+// per-matrix work counters: one pair visit (Gram / pair QR + e), and whether it rotated
+BF_DEV void bj_count(int64_t* stats, int64_t b, bool rotated) {
+  if (!stats) return;
+  atomicAdd(reinterpret_cast<unsigned long long*>(stats + 4 * b), 1ull);
+  if (rotated) atomicAdd(reinterpret_cast<unsigned long long*>(stats + 4 * b + 1), 1ull);
+}
 
 BF_DEV void bj_atomic_max_pos(double* addr, double v) {
   atomicMax((unsigned long long*)addr, (unsigned long long)__double_as_longlong(v));
@@ -113,6 +121,7 @@ __global__ void __launch_bounds__(256) bj_gram(BJGemmArgs<T> a, int step) {
     const double e = red;
     bj_atomic_max_pos(a.e_sweep + b, e);
     a.pair_act[slot] = e > a.tol ? 1 : 0;  // pairs at e <= tol are skipped (blockjacobi.py:128-129)
+    bj_count(a.stats, b, e > a.tol);
   }
 }
 
@@ -357,6 +366,7 @@ __global__ void __launch_bounds__(256) bj_gram_mma(BJGemmArgs<double> a, int ste
     const double e = red;
     bj_atomic_max_pos(a.e_sweep + b, e);
     a.pair_act[slot] = e > a.tol ? 1 : 0;  // pairs at e <= tol are skipped (blockjacobi.py:128-129)
+    bj_count(a.stats, b, e > a.tol);
   }
 }
 

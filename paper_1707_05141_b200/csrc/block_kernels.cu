@@ -13,6 +13,10 @@
 //           (blockjacobi.py:135-143).
 // A per-sweep finalize kernel records e_history, counts the sweep and retires converged
 // matrices (blockjacobi.py:150-154); converged matrices simply stop (per-matrix, :171-174).
+#include <mutex>
+#include <utility>
+#include <vector>
+
 #include "internal.h"
 #include "jacobi_cta.cuh"
 #include "qr_cta.cuh"
@@ -35,6 +39,9 @@ struct BJArgs {
   int max_sweeps;
   double tol, tol_inner;
   bool p_in_smem;
+  int64_t* stats;   // batch x 4 work counters or null (BlockLaunch::stats)
+  int32_t* in_sw;   // batched pipelines: per-slot accumulated inner-SVD sweeps
+  int64_t* in_rot;  // ... and inner-SVD rotations
 };
 
 BF_DEV void atomic_max_pos(double* addr, double v) {
@@ -159,10 +166,18 @@ __global__ void __launch_bounds__(256) bj_gram_step(BJArgs<T> a, int step) {
   __syncthreads();
   // ---- convergence measure before the update (blockjacobi.py:126-129)
   double e = scaled_offdiag_cta<T>(G, kk, kk, red);
-  if (tid == 0) atomic_max_pos(a.e_sweep + b, e);
+  if (tid == 0) {
+    atomic_max_pos(a.e_sweep + b, e);
+    bj_count(a.stats, b, e > a.tol);
+  }
   if (e <= a.tol) return;
   // ---- inner round-robin SVD of G without V (blockjacobi.py:130, _inner_options :79-81)
-  jacobi_sweeps<T, 4>(G, kk, (T*)nullptr, kk, kk, kk, kk, 1, a.tol_inner, 30, counters);
+  const SweepStats ist = jacobi_sweeps<T, 4>(G, kk, (T*)nullptr, kk, kk, kk, kk, 1, a.tol_inner, 30, counters);
+  if (tid == 0 && a.stats) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.stats + 4 * b + 2),
+              (unsigned long long)ist.sweeps * (unsigned long long)(kk * (kk - 1) / 2));
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.stats + 4 * b + 3), (unsigned long long)ist.rotations);
+  }
   extract_svd_cta<T>(G, kk, (const T*)nullptr, kk, kk, kk, kk, 0, U, kk, sig, (T*)nullptr, kk, chunk, order, cand,
                      counters + 2);
   // (extract used `chunk` as its unsorted-norm scratch; `sig` holds the sorted sigma)
@@ -207,9 +222,17 @@ __global__ void __launch_bounds__(256) bj_direct_step(BJArgs<T> a, int step) {
   }
   __syncthreads();
   double e = scaled_offdiag_cta<T>(Rw, kk, kk, red);
-  if (tid == 0) atomic_max_pos(a.e_sweep + b, e);
+  if (tid == 0) {
+    atomic_max_pos(a.e_sweep + b, e);
+    bj_count(a.stats, b, e > a.tol);
+  }
   if (e <= a.tol) return;
-  jacobi_sweeps<T, 4>(Rw, kk, Vi, kk, kk, kk, kk, 1, a.tol_inner, 30, counters);
+  const SweepStats ist = jacobi_sweeps<T, 4>(Rw, kk, Vi, kk, kk, kk, kk, 1, a.tol_inner, 30, counters);
+  if (tid == 0 && a.stats) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.stats + 4 * b + 2),
+              (unsigned long long)ist.sweeps * (unsigned long long)(kk * (kk - 1) / 2));
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.stats + 4 * b + 3), (unsigned long long)ist.rotations);
+  }
   extract_svd_cta<T>(Rw, kk, Vi, kk, kk, kk, kk, kk, Ur, kk, sig2, Vr, kk, sig, order, cand, counters + 2);
   // new pair = H_0 ... H_{kk-1} [U_R diag(sigma); 0]  (== (Q @ U_R) * sigma, blockjacobi.py:143)
   for (int e2 = tid; e2 < m * kk; e2 += blockDim.x) {
@@ -304,6 +327,7 @@ __global__ void __launch_bounds__(256) bj_dqr(BJArgs<double> a, BDArgs d, int st
   if (tid == 0) {
     atomic_max_pos(a.e_sweep + b, red[0]);
     d.pact[slot] = red[0] > a.tol ? 1 : 0;
+    bj_count(a.stats, b, red[0] > a.tol);
   }
 }
 
@@ -474,6 +498,7 @@ __global__ void __launch_bounds__(256, 1) bj_dqr_reg(BJArgs<double> a, BDArgs d,
   if (tid == 0) {
     atomic_max_pos(a.e_sweep + b, red[0]);
     d.pact[slot] = red[0] > a.tol ? 1 : 0;
+    bj_count(a.stats, b, red[0] > a.tol);
   }
 }
 
@@ -718,24 +743,103 @@ __global__ void bj_init(BJArgs<T> a, const T* A) {
     a.sweeps[b] = 0;
     a.conv[b] = 0;
   }
+  if (a.stats && threadIdx.x < 4) a.stats[4 * b + threadIdx.x] = 0;
+  if (a.in_sw)  // per-slot inner counters of this matrix's pairs
+    for (int p = threadIdx.x; p < a.nb / 2; p += blockDim.x) {
+      a.in_sw[b * (a.nb / 2) + p] = 0;
+      a.in_rot[b * (a.nb / 2) + p] = 0;
+    }
+}
+
+// fold the per-slot inner-SVD counters of the batched pipelines into the per-matrix stats
+template <typename T>
+__global__ void bj_stats_reduce(BJArgs<T> a) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= a.batch) return;
+  const int P = a.nb / 2, kk = 2 * a.k;
+  long long sw = 0, rot = 0;
+  for (int p = 0; p < P; ++p) {
+    sw += a.in_sw[b * P + p];
+    rot += a.in_rot[b * P + p];
+  }
+  a.stats[4 * b + 2] += sw * (long long)(kk * (kk - 1) / 2);
+  a.stats[4 * b + 3] += rot;
 }
 
 template <typename T>
-__global__ void bj_finalize_sweep(BJArgs<T> a) {
+__global__ void bj_finalize_sweep(BJArgs<T> a, int* still_active) {
   int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= a.batch || !a.active[b]) return;
-  double e = a.e_sweep[b];
-  int s = a.sweeps[b];
-  if (a.e_hist) a.e_hist[b * a.max_sweeps + s] = (T)e;
-  s += 1;
-  a.sweeps[b] = s;
-  if (e < a.tol) {
-    a.conv[b] = 1;
-    a.active[b] = 0;
-  } else if (s >= a.max_sweeps) {
-    a.active[b] = 0;
+  bool act = false;
+  if (b < a.batch && a.active[b]) {
+    double e = a.e_sweep[b];
+    int s = a.sweeps[b];
+    if (a.e_hist) a.e_hist[b * a.max_sweeps + s] = (T)e;
+    s += 1;
+    a.sweeps[b] = s;
+    if (e < a.tol) {
+      a.conv[b] = 1;
+      a.active[b] = 0;
+    } else if (s >= a.max_sweeps) {
+      a.active[b] = 0;
+    } else {
+      act = true;
+    }
+    a.e_sweep[b] = 0.0;
   }
-  a.e_sweep[b] = 0.0;
+  // matrices still sweeping after this sweep: the host stops enqueueing sweeps at zero
+  const unsigned bal = __ballot_sync(0xffffffffu, act);
+  if ((threadIdx.x & 31) == 0 && bal) atomicAdd(still_active, __popc(bal));
+}
+
+// Host-side sweep control: after each sweep the count of still-active matrices is copied to
+// pinned memory; the host, running up to kSweepLag sweeps ahead of the device, stops enqueueing
+// once a completed sweep reports zero (blockjacobi.py:150-154: converged matrices stop; the
+// batch stops when all have). The device never waits on the host. A call's counters may still be
+// in flight when it returns (asynchronous stream semantics), so each call takes a ring that no
+// pending copy targets: rings are pooled per device and reused once their events have completed.
+constexpr int kSweepLag = 2, kCtlRing = 4;
+struct SweepCtl {
+  int* host = nullptr;  // pinned, kCtlRing counters
+  cudaEvent_t ev[kCtlRing] = {};
+  bool recorded[kCtlRing] = {};
+  bool in_use = false;  // a call is enqueueing with this ring
+  bool idle() {
+    if (in_use) return false;
+    for (int i = 0; i < kCtlRing; ++i)
+      if (recorded[i] && cudaEventQuery(ev[i]) != cudaSuccess) return false;
+    return true;
+  }
+};
+static std::mutex g_ctl_mu;
+static SweepCtl* sweep_ctl_acquire() {
+  static std::vector<std::pair<int, SweepCtl*>> pool;  // (device, ring); rings live for the process
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_ctl_mu);
+  for (auto& e : pool)
+    if (e.first == dev && e.second->idle()) {
+      cudaGetLastError();  // clear cudaErrorNotReady from the queries
+      for (int i = 0; i < kCtlRing; ++i) e.second->recorded[i] = false;
+      e.second->in_use = true;
+      return e.second;
+    }
+  cudaGetLastError();
+  SweepCtl* c = new SweepCtl();
+  bool good = cudaMallocHost((void**)&c->host, sizeof(int) * kCtlRing) == cudaSuccess;
+  for (int i = 0; good && i < kCtlRing; ++i)
+    good = cudaEventCreateWithFlags(&c->ev[i], cudaEventDisableTiming) == cudaSuccess;
+  if (!good) {
+    cudaGetLastError();
+    return nullptr;  // fall back to max_sweeps launches
+  }
+  c->in_use = true;
+  pool.emplace_back(dev, c);
+  return c;
+}
+static void sweep_ctl_release(SweepCtl* c) {
+  if (!c) return;
+  std::lock_guard<std::mutex> lk(g_ctl_mu);
+  c->in_use = false;
 }
 
 template <typename T>
@@ -812,6 +916,7 @@ __global__ void __launch_bounds__(256) bw_offdiag(BJArgs<T> a, BWArgs<T> w, int 
   if (threadIdx.x == 0) {
     atomic_max_pos(a.e_sweep + b, e);
     w.pact[slot] = e > a.tol ? 1 : 0;
+    bj_count(a.stats, b, e > a.tol);
   }
 }
 
@@ -866,7 +971,7 @@ static size_t direct_smem(int m, int kk, bool p_in) {
 
 template <typename T>
 struct BJLayout {
-  size_t w, v, p, e, act, cand, g, u, s, pact, iws, dp, dtau, dvr, total;
+  size_t w, v, p, e, act, cand, g, u, s, pact, iws, dp, dtau, dvr, isw, irot, ring, total;
   // wide pairs (2k > 64)
   size_t xp, xpv, xq, xvr, xpn, xpvn, xqws;
 };
@@ -949,6 +1054,12 @@ static BJLayout<T> bj_layout(int64_t batch, int m, int n, int bw, int method, bo
     L.xqws = off;
     off += method == 1 ? al(qr_global_ws_bytes(es == 8 ? 0 : 1, slots, m, kk)) : 0;
   }
+  L.ring = off;
+  off += al(sizeof(int) * 4);
+  L.isw = off;
+  off += al((size_t)slots * sizeof(int32_t));
+  L.irot = off;
+  off += al((size_t)slots * sizeof(int64_t));
   L.iws = off;
   off += (bt || wide) ? al(svd_global_ws_bytes(es == 8 ? 0 : 1, slots, kk, kk, 1, bd || (wide && method == 1 && accv),
                                                0, 30))
@@ -992,6 +1103,9 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
   a.max_sweeps = L.max_sweeps;
   a.tol = L.tol;
   a.tol_inner = sizeof(T) == 8 ? Tol<double>::svd : Tol<float>::svd;
+  a.stats = L.stats;
+  a.in_sw = L.stats ? (int32_t*)(base + lay.isw) : nullptr;
+  a.in_rot = L.stats ? (int64_t*)(base + lay.irot) : nullptr;
   const int kk = 2 * k;
   a.p_in_smem = direct_smem<T>(L.m, kk, true) <= 227 * 1024;
   cudaError_t e;
@@ -1055,6 +1169,10 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
     in.tier = 0;
     in.transpose_a = false;
     in.active = g.pair_act;
+    in.sweeps = a.in_sw;  // per-slot work counters, accumulated over the run
+    in.rotations = a.in_rot;
+    in.accumulate = true;
+    g.stats = L.stats;
     rot_smem = (size_t)2 * kk * (kk + 1) * sizeof(T);
     const int TT = kk / 16;
     if (TT == 1) e = cudaFuncSetAttribute(bj_rot<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rot_smem);
@@ -1100,6 +1218,9 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
     in.tier = 0;
     in.transpose_a = false;
     in.active = dd.pact;
+    in.sweeps = a.in_sw;
+    in.rotations = a.in_rot;
+    in.accumulate = true;
     // V pair <- V pair @ V_R on the FP64 tensor cores (blockjacobi.py:146-149)
     gv.batch = L.batch;
     gv.m = L.m;
@@ -1160,10 +1281,27 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
     win.tier = 0;
     win.transpose_a = false;
     win.active = wa.pact;
+    win.sweeps = a.in_sw;
+    win.rotations = a.in_rot;
+    win.accumulate = true;
   }
   void* iws = base + lay.iws;
   const size_t iws_bytes = lay.total - lay.iws;
+  // sweep control (see SweepCtl): inside a stream capture the host cannot observe the device,
+  // so the graph gets all max_sweeps sweeps (converged matrices exit each kernel at once)
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cap);
+  SweepCtl* ctl = cap == cudaStreamCaptureStatusNone ? sweep_ctl_acquire() : nullptr;
+  struct CtlGuard {
+    SweepCtl* c;
+    ~CtlGuard() { sweep_ctl_release(c); }
+  } ctl_guard{ctl};
+  int* ring = (int*)(base + lay.ring);
   for (int sw = 0; sw < L.max_sweeps; ++sw) {
+    if (ctl && sw >= kSweepLag) {
+      const int r = (sw - kSweepLag) % kCtlRing;
+      if (cudaEventSynchronize(ctl->ev[r]) == cudaSuccess && ctl->host[r] == 0) break;
+    }
     for (int s = 0; s < nb - 1; ++s) {
       if (wide) {
         const int dt = sizeof(T) == 8 ? 0 : 1;
@@ -1223,8 +1361,16 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
         bj_direct_step<T><<<grid, 256, smem, st>>>(a, s);
       }
     }
-    bj_finalize_sweep<T><<<(unsigned)((L.batch + 255) / 256), 256, 0, st>>>(a);
+    int* cnt = ring + sw % kCtlRing;
+    cudaMemsetAsync(cnt, 0, sizeof(int), st);
+    bj_finalize_sweep<T><<<(unsigned)((L.batch + 255) / 256), 256, 0, st>>>(a, cnt);
+    if (ctl) {
+      cudaMemcpyAsync(ctl->host + sw % kCtlRing, cnt, sizeof(int), cudaMemcpyDeviceToHost, st);
+      cudaEventRecord(ctl->ev[sw % kCtlRing], st);
+      ctl->recorded[sw % kCtlRing] = true;
+    }
   }
+  if (L.stats && (bg || bd || wide)) bj_stats_reduce<T><<<(unsigned)((L.batch + 255) / 256), 256, 0, st>>>(a);
   if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
   size_t xs = (size_t)np * (sizeof(T) + sizeof(int)) + 16;
   e = cudaFuncSetAttribute(bj_extract<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xs);

@@ -38,6 +38,7 @@ struct SvdLaunch {
   int max_sweeps, ordering, tier;
   bool transpose_a;  // read A^T (a is n x m column-major) -- used by rsvd for R_B^T
   const uint8_t* active = nullptr;  // optional per-entry mask: inactive entries are skipped
+  bool accumulate = false;          // add to sweeps / rotations instead of storing (block inner SVDs)
 };
 
 struct GemmLaunch {
@@ -85,6 +86,10 @@ struct BlockLaunch {
   void* e_history;  // batch x max_sweeps or null
   int block_width, method, max_sweeps;
   double tol;
+  // optional per-matrix work counters (batch x 4): pair visits (Gram / pair QR + e), rotated pairs,
+  // inner-SVD pair visits (inner sweeps x 2k(2k-1)/2), inner-SVD rotations -- the run's own counts
+  // behind the algorithmic flop figure
+  int64_t* stats = nullptr;
 };
 size_t block_ws_bytes(int dtype, int64_t batch, int m, int n, int block_width, int method, bool accv);
 int launch_block_svd(int dtype, const BlockLaunch& L, void* ws, cudaStream_t st);

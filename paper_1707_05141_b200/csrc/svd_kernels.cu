@@ -25,6 +25,7 @@ struct SvdArgs {
   int32_t* sweeps;
   uint8_t* conv;
   int64_t* rots;
+  bool accum;  // += into sweeps / rots (block inner SVDs)
   double tol;
   int max_sweeps, ordering;
   bool in_smem;
@@ -108,9 +109,9 @@ BF_DEV void svd_cta_body(const SvdArgs<T>& a, unsigned char* smem_raw, int64_t b
   extract_svd_cta<T>(W, m, V, nw, m, n, n, n, a.u + b * a.u_stride, m, a.s + b * a.s_stride,
                      accv ? a.v + b * a.v_stride : nullptr, n, sig, order, cand, counters + 2);
   if (tid == 0) {
-    if (a.sweeps) a.sweeps[b] = st.sweeps;
+    if (a.sweeps) a.sweeps[b] = (a.accum ? a.sweeps[b] : 0) + st.sweeps;
     if (a.conv) a.conv[b] = (uint8_t)st.converged;
-    if (a.rots) a.rots[b] = st.rotations;
+    if (a.rots) a.rots[b] = (a.accum ? a.rots[b] : 0) + st.rotations;
   }
 }
 
@@ -183,6 +184,7 @@ static int launch_svd_t(const SvdLaunch& L, void* ws, cudaStream_t st) {
   a.sweeps = L.sweeps;
   a.conv = L.converged;
   a.rots = L.rotations;
+  a.accum = L.accumulate;
   a.tol = L.tol;
   a.max_sweeps = L.max_sweeps;
   a.ordering = L.ordering;

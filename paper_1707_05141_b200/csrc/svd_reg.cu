@@ -29,6 +29,7 @@ struct RegArgs {
   int32_t* sweeps;
   uint8_t* conv;
   int64_t* rots;
+  bool accum;  // += into sweeps / rots (block inner SVDs)
   double tol;
   int max_sweeps;
   double2* log;  // gridDim.x slots of log_stride entries (null without V)
@@ -133,9 +134,9 @@ __global__ void __launch_bounds__(C::threads, BF_REG_MINB) svd_reg_kernel(RegArg
     extract_svd_cta<T>(Wsm, m, nullptr, nw, m, n, n, 0, a.u + b * a.u_stride, m, a.s + b * a.s_stride, nullptr, n,
                        sig, order, cand, ctr + 6);
     if (tid == 0) {
-      if (a.sweeps) a.sweeps[b] = act.sweeps;
+      if (a.sweeps) a.sweeps[b] = (a.accum ? a.sweeps[b] : 0) + act.sweeps;
       if (a.conv) a.conv[b] = (uint8_t)conv;
-      if (a.rots) a.rots[b] = act.rots;
+      if (a.rots) a.rots[b] = (a.accum ? a.rots[b] : 0) + act.rots;
     }
     if (accv) {
       // ---- V: identity, replay the log, write in sorted order
@@ -251,6 +252,7 @@ static int launch_reg(const SvdLaunch& L, void* ws, size_t ws_bytes, cudaStream_
   a.sweeps = L.sweeps;
   a.conv = L.converged;
   a.rots = L.rotations;
+  a.accum = L.accumulate;
   a.tol = L.tol;
   a.max_sweeps = L.max_sweeps;
   a.log = L.v ? (double2*)ws : nullptr;

@@ -481,6 +481,7 @@ struct RRArgs {
   int32_t* sweeps;
   uint8_t* conv;
   int64_t* rots;
+  bool accum;  // += into sweeps / rots (block inner SVDs)
   double tol;
   int max_sweeps;
   double2* log;
@@ -579,9 +580,9 @@ __global__ void __launch_bounds__(C::THREADS, BF_RR_MINB) svd_rr_kernel(RRArgs<d
     extract_svd_cta<double>(Wsm, m, nullptr, nw, m, n, n, 0, a.u + b * a.u_stride, m, a.s + b * a.s_stride, nullptr, n,
                             sig, order, cand, ctr + 6);
     if (tid == 0) {
-      if (a.sweeps) a.sweeps[b] = wk.sweeps;
+      if (a.sweeps) a.sweeps[b] = (a.accum ? a.sweeps[b] : 0) + wk.sweeps;
       if (a.conv) a.conv[b] = (uint8_t)conv;
-      if (a.rots) a.rots[b] = wk.rots;
+      if (a.rots) a.rots[b] = (a.accum ? a.rots[b] : 0) + wk.rots;
     }
     if (accv && a.split_v) {
       int32_t* vm = a.vmeta + b * (int64_t)(nw + 1);
@@ -722,6 +723,7 @@ static int launch_rr(const SvdLaunch& L, int nw, void* ws, size_t ws_bytes, cuda
   a.sweeps = L.sweeps;
   a.conv = L.converged;
   a.rots = L.rotations;
+  a.accum = L.accumulate;
   a.tol = L.tol;
   a.max_sweeps = L.max_sweeps;
   a.log = L.v ? (double2*)ws : nullptr;
