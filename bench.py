@@ -5,9 +5,11 @@ python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--c
 One "step" = one pass of the hot path over the config's whole batch (synthetic inputs of
 the BASELINE shape, generated on the device with the reference's Gaussian stream).
 Headline workload (N=1): cfg3, 5,000 random 64x64 fp64 matrices, round-robin Jacobi with V
-(the shared-memory tier). The other BASELINE configs are measured in the same run under
-"configs" (fewer steps). Multi-GPU (torchrun): every rank runs its own full batch (weak
-scaling, no data-path collective); time = max over ranks of the device time.
+(the shared-memory tier). Every other BASELINE config is measured in the same run under
+"configs" with the same fields (device value, roofline, e2e through host buffers, CPU baseline,
+launch count). Multi-GPU: `--gpus N` launches N ranks itself (torch.distributed.run) when not
+already under torchrun; --scaling weak (default: every rank its own full batch) or strong (the
+config's batch split over the ranks); no data-path collective; time = max over ranks.
 
 --impl reference times the CPU oracle (oracle/: the reference algorithm restated in C,
 since the reference itself is pure Python and cannot travel) on all host cores, rank 0 only.
@@ -152,10 +154,32 @@ class ClockSampler:
 # ----------------------------------------------------------------- GPU arm
 
 
-class GpuConfig:
-    """Builds device-resident inputs for one config and runs its hot path once per step."""
+def block_flops(m, n, kk, method, stats, accv=True):
+    """cfg4/cfg4d algorithmic flops from the run's own per-matrix counters (bf_block_svd_batched_ex:
+    pair visits, rotated pairs, inner pair visits, inner rotations), SURVEY §8d conventions:
+    Gram: 2m(2k)^2 per visited pair (G = P^T P), (2m + 2n)(2k)^2 per rotated pair (P U, V_pair U);
+    direct: QR 4m(2k)^2 - 4(2k)^3/3 per visit, (2m + 2n)(2k)^2 per rotated pair (Q [U S; 0], V_pair V_R);
+    inner Jacobi: 6(2k) per inner pair visit, 6(2k) (+6(2k) with V, direct) per inner rotation."""
+    s = stats.double().sum(dim=0).tolist()
+    visits, rotated, ivisits, irot = s
+    if method == "gram":
+        outer = visits * 2.0 * m * kk * kk + rotated * (2.0 * m + (2.0 * n if accv else 0.0)) * kk * kk
+        inner = 6.0 * kk * ivisits + 6.0 * kk * irot
+    else:
+        outer = visits * (4.0 * m * kk * kk - 4.0 * kk ** 3 / 3.0) + rotated * (2.0 * m + (2.0 * n if accv else 0.0)) * kk * kk
+        inner = 6.0 * kk * ivisits + 12.0 * kk * irot
+    return outer + inner, {"pair_visits": visits, "rotated_pairs": rotated, "inner_pair_visits": ivisits,
+                           "inner_rotations": irot}
 
-    def __init__(self, name, cfg, device, rank, world=1):
+
+class GpuConfig:
+    """Builds device-resident inputs for one config and runs its hot path once per step.
+
+    scaling "weak": every rank owns `batch` entries of a world*batch global batch; "strong": the
+    config's batch is split over the ranks. Either way a rank's entries are a contiguous shard with
+    its global index_base (rsvd's seed ^ i stays global, rsvd.py:82-85)."""
+
+    def __init__(self, name, cfg, device, rank, world=1, scaling="weak", batch=None):
         import torch
 
         from paper_1707_05141_b200.shard import ShardPlan
@@ -169,15 +193,17 @@ class GpuConfig:
         self.k_svd, self.k_qr, self.k_block, self.k_rsvd = svd_colmajor, qr_colmajor, block_svd_colmajor, rsvd_colmajor
         self.bf, self.torch = bf, torch
         self.name, self.cfg, self.dev = name, cfg, device
-        m, n, B = cfg["m"], cfg["n"], cfg["batch"]
-        # weak scaling: a global batch of world*B entries, contiguous shard of B per rank
-        self.plan = ShardPlan(world * B, world, rank)
+        m, n = cfg["m"], cfg["n"]
+        B = cfg["batch"] if batch is None else batch
+        self.global_batch = world * B if scaling == "weak" else B
+        self.plan = ShardPlan(self.global_batch, world, rank)
+        self.local_batch = self.plan.count
         seed0 = cfg["seed"] + self.plan.start
         if cfg["kind"] == "rsvd":
-            self.a, _ = bf.make_matrix_tensor(B, m, n, 1e16, rank=64, seed=cfg["seed"], index_base=self.plan.start,
-                                              device=device)
+            self.a, _ = bf.make_matrix_tensor(self.local_batch, m, n, 1e16, rank=64, seed=cfg["seed"],
+                                              index_base=self.plan.start, device=device)
         else:
-            self.a = bf.gaussian_tensor(B, m, n, seed0, seed_mode="add", device=device)
+            self.a = bf.gaussian_tensor(self.local_batch, m, n, seed0, seed_mode="add", device=device)
         self.store = self.a.transpose(1, 2).contiguous()  # column-major storage, resident
         torch.cuda.synchronize(device)
         self.out = None
@@ -191,8 +217,7 @@ class GpuConfig:
         elif c["kind"] == "qr":
             self.out = self.k_qr(self.store, m, n, 16)
         elif c["kind"] == "block":
-            opts = block_opts(c)
-            self.out = self.k_block(self.store, m, n, opts)
+            self.out = self.k_block(self.store, m, n, block_opts(c), stats=True)
         else:
             opts = bf.RsvdOptions(k=c["k"], p=c["p"], seed=5)
             self.out = self.k_rsvd(self.store, m, n, opts, index_base=self.plan.start)  # seed ^ global index
@@ -206,41 +231,25 @@ class GpuConfig:
         return {"qr": "qr_reg_kernel", "block": "bj_gram_mma + svd_rr_kernel (inner) + bj_rot_mma",
                 "rsvd": "gemm_mma_kernel + qr_reg_kernel + svd_rr_kernel + svd_rr_vkernel"}[c["kind"]]
 
-    def launches_per_step(self):
-        """Our kernels per step, as the ncu launch lists show them (profiles/launches_r01.md)."""
+    def work(self):
+        """(algorithmic flops, compulsory bytes, counters) of the last step, from the run's own
+        sweep / rotation / pair counters."""
         c = self.cfg
-        if c["kind"] == "svd":
-            return 2 if c["ordering"] == "round_robin" else 1  # sweep kernel + V replay kernel
-        if c["kind"] == "qr":
-            return 1
-        if c["kind"] == "block":
-            nb = c["n"] // 32
-            # init + 30 sweeps (launched unconditionally; converged entries exit at once) x (steps x
-            # kernels + finalize) + extract. Gram: gram, inner svd (U only), rotation; direct: pair
-            # QR, inner svd sweep + V replay, WY apply, V-pair rotation
-            per = 3 if c.get("method", "gram") == "gram" else 5
-            return 2 + 30 * (per * (nb - 1) + 1)
-        return 10  # rsvd: gaussian, 4 DMMA gemms, 2 qr, svd sweep + V replay, sign fix
-
-    def flops(self):
-        """Algorithmic flops of the last step (counted from the run's own sweep/rotation counters)."""
-        c = self.cfg
-        m, n, B = c["m"], c["n"], c["batch"]
+        m, n, B = c["m"], c["n"], self.local_batch
         if c["kind"] == "svd":
             sw = self.out["sweeps"].double().sum().item()
             rot = self.out["rotations"].double().sum().item()
-            return jacobi_flops(m, n, sw, rot), B * 8.0 * (2 * m * n + n * n + n)
+            return (jacobi_flops(m, n, sw, rot), B * 8.0 * (2 * m * n + n * n + n),
+                    {"sweeps_mean": sw / max(B, 1), "rotations_mean": rot / max(B, 1)})
         if c["kind"] == "qr":
-            return B * qr_flops(m, n), B * 8.0 * (2 * m * n + n * n)
+            return B * qr_flops(m, n), B * 8.0 * (2 * m * n + n * n), {}
         if c["kind"] == "block":
-            # Gram'd pairs: 2m(2k)^2 each; rotations: (2m + 2n)(2k)^2; inner SVD ~ oracle nominal 1.33 GFLOP/matrix
-            sw = self.out["sweeps"].double().sum().item()
-            k2 = 64
-            pairs = sw * 28
-            f = pairs * (2.0 * m * k2 * k2 + (2.0 * m + 2.0 * n) * k2 * k2) + B * 1.33e9
-            return f, B * 8.0 * (3 * m * n + n)
+            f, cnt = block_flops(m, n, 64, c.get("method", "gram"), self.out["stats"])
+            cnt["sweeps_mean"] = self.out["sweeps"].double().mean().item()
+            return f, B * 8.0 * (3 * m * n + n), cnt
         w = c["k"] + c["p"]
-        return B * rsvd_flops(m, n, w, 2.909e6), B * 8.0 * (m * n + m * w + n * w + w)
+        return (B * rsvd_flops(m, n, w, 2.909e6), B * 8.0 * (m * n + m * w + n * w + w),
+                {"inner_svd": "oracle-mean nominal 2.909 MFLOP per 40x40 inner SVD with V"})
 
     def device_op(self):
         """The config's batched call as op(dev_store, index_base) -> output tensors (C-ABI call)."""
@@ -278,6 +287,40 @@ class GpuConfig:
                            index_base=self.plan.start, taper=chunks > 0)
         return sum(o.numel() * o.element_size() for o in pinned_out)
 
+    def dropin_call(self, host_list):
+        """The reference-shaped drop-in call: list of numpy matrices in, list of dataclasses out."""
+        bf, c = self.bf, self.cfg
+        if c["kind"] == "svd":
+            return bf.batch_svd(host_list, bf.JacobiOptions(ordering=c["ordering"], accumulate_v=True), device=self.dev)
+        if c["kind"] == "qr":
+            return bf.batch_qr(host_list, 16, device=self.dev)
+        if c["kind"] == "block":
+            return bf.batch_block_svd(host_list, block_opts(c), device=self.dev)
+        return bf.batch_rsvd(host_list, bf.RsvdOptions(k=c["k"], p=c["p"], seed=5), device=self.dev)
+
+
+def count_launches(gc):
+    """Our kernels in one step, counted by the CUDA profiler (kernel names in namespace bf::), in an
+    untimed extra step. Falls back to None when CUPTI is unavailable (e.g. under ncu)."""
+    if os.environ.get("BF_BENCH_NO_PROFILER"):
+        return None, []
+    try:
+        from torch.profiler import ProfilerActivity, profile
+
+        gc.torch.cuda.synchronize(gc.dev)
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            gc.step()
+            gc.torch.cuda.synchronize(gc.dev)
+        names = {}
+        for ev in prof.events():
+            nm = ev.name
+            if "bf::" in nm:
+                short = nm.split("bf::", 1)[1].split("<", 1)[0].split("(", 1)[0]
+                names[short] = names.get(short, 0) + 1
+        return sum(names.values()), sorted(names.items(), key=lambda kv: -kv[1])
+    except Exception:  # noqa: BLE001
+        return None, []
+
 
 def time_gpu(gc, steps, warmup, flush):
     torch = gc.torch
@@ -311,6 +354,41 @@ def time_e2e(gc, steps, chunks):
     dt = time.perf_counter() - t0
     h2d = host_in.numel() * host_in.element_size()
     return dt, h2d, d2h
+
+
+def time_dropin(gc, steps):
+    """The drop-in API on host numpy matrices (list in, dataclasses out), as a reference user calls it."""
+    host = gc.a.cpu().numpy()
+    mats = [np.asfortranarray(x) for x in host]
+    gc.dropin_call(mats[: min(len(mats), 64)])  # warm-up
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        gc.dropin_call(mats)
+    return time.perf_counter() - t0
+
+
+def roofline(gc, flops, bytes_alg, t_step, peaks, prof):
+    """Roofline object of the step: FP64 for the Jacobi / block / rsvd paths, HBM for the QR (whose
+    intensity ~5.3 flop/B sits at the FP64 ridge; both fractions are reported)."""
+    tf = flops / t_step / 1e12
+    gbs = bytes_alg / t_step / 1e9
+    common = {"kernel": gc.kernel_name(), "traffic": prof.get("dram_bytes_per_launch"),
+              "traffic_kernel": prof.get("kernel"), "traffic_source": prof.get("source"),
+              "flops_per_step": flops, "alg_bytes_per_step": bytes_alg,
+              "fp64_tflops": tf, "fp64_frac": tf / peaks["fp64_tflops"],
+              "hbm_gbs": gbs, "hbm_frac": gbs / peaks["hbm_gbs"],
+              "dfma_peak": peaks.get("fp64_dfma_tflops"),
+              "frac_of_dfma": tf / peaks["fp64_dfma_tflops"] if peaks.get("fp64_dfma_tflops") else None,
+              "flops_rule": "SURVEY §8d / PAPER.md:172 conventions, counted from the run's own per-matrix "
+                            "sweep / rotation / pair counters (rsvd: inner SVD at the oracle's mean)"}
+    if gc.cfg["kind"] == "qr":
+        return dict(bound="hbm", achieved=gbs, peak=peaks["hbm_gbs"], unit="GB/s", frac=gbs / peaks["hbm_gbs"],
+                    peak_source="MEASURED_PEAKS.json hbm_gbs (copy bandwidth on this pool)", **common)
+    return dict(bound="tensor", achieved=tf, peak=peaks["fp64_tflops"], unit="TFLOP/s",
+                frac=tf / peaks["fp64_tflops"],
+                peak_source="FP64 compute roof: FP64 tensor-core (DMMA) loop measured on this pool, "
+                            "profiles/fp64_peak_r01.json (MEASURED_PEAKS.json has no FP64 entry); the Jacobi "
+                            "kernels issue DFMA, whose measured peak is lower (dfma_peak)", **common)
 
 
 # ----------------------------------------------------------------- CPU oracle arm
@@ -383,19 +461,116 @@ def spawn_ranks(n):
     return subprocess.call(cmd)
 
 
+def measure(name, cfg, device, rank, world, args, flush, peaks, barrier, max_over_ranks, steps, warmup,
+            e2e=True, dropin=False, batch=None):
+    """One config: device-resident timing (CUDA events, max over ranks), the counted work, the
+    roofline object, the host-buffer e2e leg and (optionally) the list-in drop-in leg."""
+    torch = __import__("torch")
+    gc = GpuConfig(name, cfg, device, rank, world, args.scaling, batch=batch)
+    barrier()
+    clocks = ClockSampler(device.index)
+    clocks.start()
+    barrier()
+    t_dev = time_gpu(gc, steps, warmup, flush)
+    barrier()
+    clk = clocks.stop()
+    t_max = max_over_ranks(t_dev)
+    flops, bytes_alg, counters = gc.work()
+    t_step = t_dev / steps  # this rank's step: its flops over its own device time
+    prof = load_profile(name)
+    ent = {"value": gc.global_batch * steps / t_max, "unit": UNIT, "ms_per_step": 1e3 * t_max / steps,
+           "global_batch": gc.global_batch, "batch_per_gpu": gc.local_batch,
+           "gflops": world * flops / t_max * steps / 1e9,
+           "roofline": roofline(gc, flops, bytes_alg, t_step, peaks, prof), "counters": counters, "clocks": clk}
+    n_launch, kinds = count_launches(gc)
+    ent["gpu_launches"] = None if n_launch is None else n_launch * steps
+    ent["kernels_per_step"] = dict(kinds)
+    if e2e:
+        e2e_steps = max(3, min(steps, 5))
+        t_e2e, h2d, d2h = time_e2e(gc, e2e_steps, args.e2e_chunks)
+        t_e2e = max_over_ranks(t_e2e)
+        ent["e2e"] = {"value": gc.global_batch * e2e_steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                      "d2h_bytes_per_step": d2h,
+                      "path": "host-buffer call (paper_1707_05141_b200.stream.run_host_pipelined: one C-ABI batched "
+                              "call per chunk) with pinned HOST buffers: H2D of A, D2H of every output inside the "
+                              "timed region", "chunks": args.e2e_chunks}
+    if dropin:
+        dsteps = 2
+        t_d = max_over_ranks(time_dropin(gc, dsteps))
+        ent["e2e_dropin"] = {"value": gc.global_batch * dsteps / t_d, "unit": UNIT,
+                             "path": "drop-in API as the reference is called: batch_*(list of numpy matrices) -> "
+                                     "list of result dataclasses (host stacking, H2D, kernels, D2H, unstacking)"}
+    del gc
+    torch.cuda.empty_cache()
+    return ent
+
+
+BATCH_SWEEP = [125, 250, 500, 1000, 2000, 4000, 8000, 16000]
+
+
+def selftest(args, rank, world):
+    """Launcher / sharding check without GPUs (gloo on CPU): every rank takes its contiguous shard
+    of small cfg1- and cfg5-shaped batches under the same ShardPlan / index_base logic the GPU run
+    uses, runs the CPU oracle on it as the stand-in for the device call (test infrastructure), and
+    the all-gathered results on rank 0 must equal a single-rank run bit for bit (core.py:97-103;
+    rsvd's seed ^ global index, rsvd.py:82-85). Prints one JSON line on rank 0."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle as orc
+    from paper_1707_05141_b200.shard import ShardPlan, gather_results
+
+    if world > 1:
+        dist.init_process_group("gloo")
+    checks = {}
+    for what, (m, n, B) in (("svd", (16, 12, 37)), ("rsvd", (24, 20, 29))):
+        a3 = np.stack([orc.gaussian_matrix(m, n, 9_000_000 + i).T for i in range(B)])  # (B, n, m)
+        plan = ShardPlan(B, world, rank)
+        loc = np.ascontiguousarray(a3[plan.start:plan.stop])
+
+        def run(x, ib):
+            if what == "svd":
+                r = orc.batch_svd_stacked(x, m, n, ordering="round_robin", accumulate_v=True)
+                return {"s": torch.from_numpy(np.ascontiguousarray(r["s"])),
+                        "u": torch.from_numpy(np.ascontiguousarray(r["u"])),
+                        "sweeps": torch.from_numpy(r["sweeps"].astype(np.int32))}
+            r = orc.batch_rsvd_stacked(x, m, n, 4, 2, seed=5, index_base=ib)
+            return {"s": torch.from_numpy(np.ascontiguousarray(r["s"])),
+                    "v": torch.from_numpy(np.ascontiguousarray(r["v"]))}
+
+        got = gather_results(run(loc, plan.start), plan)
+        if rank == 0:
+            ref = run(np.ascontiguousarray(a3), 0)
+            checks[what] = {"entries": B, "shard_counts": plan.counts,
+                            "bitwise_equal": all(torch.equal(got[k], ref[k]) for k in ref)}
+    if rank == 0:
+        ok = all(c["bitwise_equal"] for c in checks.values())
+        print(json.dumps({"selftest": "ok" if ok else "FAILED", "world": world, "backend": "gloo" if world > 1 else None,
+                          "launcher": "torch.distributed.run (spawned by bench.py --gpus N)"
+                                      if os.environ.get("TORCHELASTIC_RUN_ID") else "direct",
+                          "checks": checks}))
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default=HEADLINE, help="headline config (cfg1..cfg5)")
+    ap.add_argument("--config", default=HEADLINE, help="headline config (cfg1..cfg5, cfg4d)")
     ap.add_argument("--no-extra", action="store_true", help="skip the other configs")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
-    ap.add_argument("--e2e-chunks", type=int, default=-12, help="host-buffer pipeline chunks for the e2e leg (negative: equal chunks, no taper)")
+    ap.add_argument("--no-dropin", action="store_true", help="skip the list-in drop-in e2e leg")
+    ap.add_argument("--batch-sweep", action="store_true", help="also time the headline config at several batch sizes")
+    ap.add_argument("--e2e-chunks", type=int, default=-12,
+                    help="host-buffer pipeline chunks for the e2e leg (negative: equal chunks, no taper)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every rank runs the config's full batch; strong: the config's batch is split "
                          "over the ranks (contiguous shards, index_base keeps rsvd's seed ^ i global)")
+    ap.add_argument("--selftest", action="store_true",
+                    help="CPU-only launcher/sharding check over gloo (no GPU): shard-invariant gathered results")
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         # `python bench.py --gpus N` without torchrun: launch the N ranks ourselves (one per GPU)
@@ -403,11 +578,16 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.selftest:
+        selftest(args, rank, world)
+        return
     name = args.config
     cfg = CONFIGS[name]
-    workload = {"workload": cfg["desc"], "config": name, "batch_per_gpu": cfg["batch"], "m": cfg["m"],
-                "n": cfg["n"], "l2": "flushed between timed steps (256 MiB memset)",
-                "parallelism": f"batch-sharded x{args.gpus} (weak)"}
+    gbatch = world * cfg["batch"] if args.scaling == "weak" else cfg["batch"]
+    workload = {"workload": cfg["desc"], "config": name, "global_batch": gbatch,
+                "batch_per_gpu": cfg["batch"] if args.scaling == "weak" else f"{cfg['batch']}/{world}",
+                "m": cfg["m"], "n": cfg["n"], "l2": "flushed between timed steps (256 MiB memset)",
+                "parallelism": f"batch-sharded x{world} ({args.scaling}); no data-path collective"}
 
     if args.impl == "reference":
         if rank != 0:
@@ -422,11 +602,12 @@ def main():
         v = float(np.median(vals))
         line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sample / v,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (reference Gaussian stream)", "config": workload,
                 "cpu_baseline": {"value": v, "unit": UNIT, "cores": thr, "kind": "port",
                                  "sample": f"{sample} matrices per step, oracle C restatement of the reference "
-                                           f"(pure-Python reference cannot travel), {thr} threads"},
+                                           f"(the pure-Python reference cannot travel; per core the C port is "
+                                           f"~11x faster than the as-shipped Python, DESIGN §4), {thr} threads"},
                 "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
@@ -456,84 +637,47 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    gc = GpuConfig(name, cfg, device, rank, world)
-    barrier()
-    clocks = ClockSampler(local)
-    clocks.start()
-    barrier()
-    t_dev = time_gpu(gc, args.steps, args.warmup, flush)
-    barrier()
-    clk = clocks.stop()
-    t_max = max_over_ranks(t_dev)
-    B = cfg["batch"]
-    value = world * B * args.steps / t_max
-    flops, bytes_alg = gc.flops()
-    ms = 1e3 * t_max / args.steps
-    # the headline step is one C-ABI call = the sweep kernel + the V-replay kernel back to back on
-    # the current stream; the CUDA-event time of the step is their combined duration (the sweep
-    # kernel is ~2/3 of it, profiles/launches_r01.md)
-    t_launch = t_dev / args.steps
-    achieved_tf = flops / t_launch / 1e12
-    prof = load_profile(name)
-    # e2e through the public API with host buffers
-    e2e_steps = max(5, args.steps)  # host-side timing: more steps than the device leg
-    t_e2e, h2d, d2h = time_e2e(gc, e2e_steps, args.e2e_chunks)
-    e2e_v = max_over_ranks(t_e2e)
-    e2e_value = world * B * e2e_steps / e2e_v
-
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference Gaussian stream, generated on device)",
-            "config": workload, "gflops": flops / t_launch / 1e9,
-            "roofline": {"bound": "tensor", "achieved": achieved_tf, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
-                         "frac": achieved_tf / peaks["fp64_tflops"],
-                         "traffic": prof.get("dram_bytes_per_launch"),
-                         "kernel": gc.kernel_name(),
-                         "traffic_kernel": prof.get("kernel"),
-                         "launches_per_step": gc.launches_per_step(),
-                         "flops_per_launch": flops, "alg_bytes_per_launch": bytes_alg,
-                         "peak_source": "FP64 compute roof: FP64 tensor-core (DMMA) loop measured on this pool, "
-                                        "profiles/fp64_peak_r01.json (MEASURED_PEAKS.json has no FP64 entry); the "
-                                        "Jacobi kernels issue DFMA, whose measured peak is lower",
-                         "dfma_peak": peaks.get("fp64_dfma_tflops"),
-                         "frac_of_dfma": achieved_tf / peaks["fp64_dfma_tflops"] if peaks.get("fp64_dfma_tflops") else None,
-                         "flops_rule": "SURVEY §8d / PAPER.md:172: 6m per pair visit + (6m+6n) per rotation, from the "
-                                       "run's own per-matrix sweep and rotation counters",
-                         "traffic_source": prof.get("source"),
-                         "hbm_achieved_gbs": bytes_alg / t_launch / 1e9, "hbm_peak_gbs": peaks["hbm_gbs"]},
-            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "path": "host-buffer call (paper_1707_05141_b200.stream.run_host_pipelined: one C-ABI "
-                            "bf_svd_batched_f64 call per chunk) with pinned HOST buffers: H2D of A, D2H of U, sigma, "
-                            "V, sweeps, converged inside the timed region",
-                    "chunks": args.e2e_chunks},
-            "gpu_launches": gc.launches_per_step() * args.steps, "clocks": clk}
-    del gc
-    torch.cuda.empty_cache()
+    ent = measure(name, cfg, device, rank, world, args, flush, peaks, barrier, max_over_ranks, args.steps,
+                  args.warmup, e2e=True, dropin=not args.no_dropin)
+    line = {"metric": METRIC, "value": ent["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ent["ms_per_step"], "higher_is_better": True,
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference Gaussian stream, generated on device)", "config": workload,
+            "gflops": ent["gflops"], "roofline": ent["roofline"], "e2e": ent["e2e"],
+            "gpu_launches": ent["gpu_launches"], "kernels_per_step": ent["kernels_per_step"],
+            "counters": ent["counters"], "clocks": ent["clocks"]}
+    if "e2e_dropin" in ent:
+        line["e2e_dropin"] = ent["e2e_dropin"]
 
     if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_baseline(name, cfg, host_threads())
+        cb = cpu_baseline(name, cfg, host_threads())
+        line["cpu_baseline"] = cb
+        line["vs_cpu_baseline"] = {"value": ent["value"] / cb["value"], "e2e": ent["e2e"]["value"] / cb["value"]}
+
+    if args.batch_sweep:
+        sweep = {}
+        for bsz in BATCH_SWEEP:
+            e = measure(name, cfg, device, rank, world, args, flush, peaks, barrier, max_over_ranks, 3, 2,
+                        e2e=False, batch=bsz)
+            sweep[str(bsz)] = {"value": e["value"], "ms_per_step": e["ms_per_step"],
+                               "frac": e["roofline"]["frac"], "bound": e["roofline"]["bound"]}
+        line["batch_sweep"] = sweep
 
     if not args.no_extra:
         extra = {}
         for other, oc in CONFIGS.items():
             if other == name:
                 continue
-            g2 = GpuConfig(other, oc, device, rank, world)
-            barrier()
             st = 2 if oc["kind"] == "block" else 3
-            t2 = time_gpu(g2, st, 3, flush)
-            t2m = max_over_ranks(t2)
-            f2, b2 = g2.flops()
-            ent = {"desc": oc["desc"], "value": world * oc["batch"] * st / t2m, "unit": UNIT,
-                   "ms_per_step": 1e3 * t2m / st, "gflops": f2 / (t2 / st) / 1e9,
-                   "fp64_frac": f2 / (t2 / st) / 1e12 / peaks["fp64_tflops"],
-                   "hbm_frac": b2 / (t2 / st) / 1e9 / peaks["hbm_gbs"]}
-            del g2
-            torch.cuda.empty_cache()
+            e = measure(other, oc, device, rank, world, args, flush, peaks, barrier, max_over_ranks, st, 2,
+                        e2e=True)
+            e["desc"] = oc["desc"]
+            e.pop("clocks", None)
             if rank == 0 and world == 1 and not args.no_cpu:
                 cb = cpu_baseline(other, oc, host_threads())
-                ent["cpu_baseline"] = cb
-            extra[other] = ent
+                e["cpu_baseline"] = cb
+                e["vs_cpu_baseline"] = {"value": e["value"] / cb["value"], "e2e": e["e2e"]["value"] / cb["value"]}
+            extra[other] = e
         line["configs"] = extra
     if rank == 0:
         print(json.dumps(line))

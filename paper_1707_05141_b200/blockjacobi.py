@@ -21,6 +21,8 @@ from .core import (
     group_entries,
     ptr,
     resolve_device,
+    resolve_devices,
+    run_sharded,
     stack_to_device,
     stream_handle,
     to_host,
@@ -125,29 +127,31 @@ def block_svd_tensor(a, opts=None, *, stats=False):
     )
 
 
-def batch_block_svd(batch, opts=None, *, threads=1, device=None):
-    """Per-entry :func:`block_svd` (blockjacobi.py:171-174); converged entries simply stop."""
+def batch_block_svd(batch, opts=None, *, threads=1, device=None, devices=None):
+    """Per-entry :func:`block_svd` (blockjacobi.py:171-174); converged entries simply stop.
+    ``devices`` shards the batch over several GPUs."""
     del threads
     opts = opts or BlockJacobiOptions()
-    dev = resolve_device(device)
+    devs = resolve_devices(device, devices)
     groups, mats = group_entries(batch, _validate)
     out = [None] * len(mats)
     for (m, n, _), idx in groups.items():
-        store = stack_to_device(mats, idx, dev)
-        r = block_svd_colmajor(store, m, n, opts)
-        uh, sh = to_host(r["u"]), to_host(r["s"])
-        vh = to_host(r["v"]) if r["v"] is not None else None
-        swh, cvh, ehh = to_host(r["sweeps"]), to_host(r["converged"]), to_host(r["e_history"])
-        for j, i in enumerate(idx):
-            sw = int(swh[j])
-            out[i] = BlockSvdResult(
-                u=np.asfortranarray(uh[j].T),
-                sigma=sh[j].copy(),
-                v=None if vh is None else np.asfortranarray(vh[j].T),
-                converged=bool(cvh[j]),
-                sweeps=sw,
-                e_history=[float(x) for x in ehh[j, :sw]],
-            )
+        def launch(store, dev, off):
+            r = block_svd_colmajor(store, m, n, opts)
+            return {"u": r["u"], "s": r["s"], "v": r["v"], "sweeps": r["sweeps"], "conv": r["converged"],
+                    "eh": r["e_history"]}
+
+        for piece, h in run_sharded(mats, idx, devs, launch):
+            for j, i in enumerate(piece):
+                sw = int(h["sweeps"][j])
+                out[i] = BlockSvdResult(
+                    u=np.asfortranarray(h["u"][j].T),
+                    sigma=h["s"][j].copy(),
+                    v=None if h["v"] is None else np.asfortranarray(h["v"][j].T),
+                    converged=bool(h["conv"][j]),
+                    sweeps=sw,
+                    e_history=[float(x) for x in h["eh"][j, :sw]],
+                )
     return out
 
 

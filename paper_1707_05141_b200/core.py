@@ -62,6 +62,51 @@ def resolve_device(device=None):
     return device
 
 
+def resolve_devices(device=None, devices=None):
+    """The devices of a drop-in call: ``devices`` (the batch is sharded over them, SURVEY §8b
+    "devices= selects GPUs for sharding") or the single ``device``."""
+    if devices is None:
+        return [resolve_device(device)]
+    if device is not None:
+        raise ValueError("pass device or devices, not both")
+    devs = [resolve_device(d) for d in devices]
+    if not devs:
+        raise ValueError("devices must name at least one CUDA device")
+    return devs
+
+
+def split_contiguous(idx, parts):
+    """Cut an index list into ``parts`` contiguous pieces (the ShardPlan split: the first
+    len % parts pieces one longer); returns [(offset_in_idx, piece)], empty pieces dropped."""
+    n = len(idx)
+    base, extra = divmod(n, parts)
+    out, start = [], 0
+    for r in range(parts):
+        cnt = base + (1 if r < extra else 0)
+        if cnt:
+            out.append((start, idx[start:start + cnt]))
+        start += cnt
+    return out
+
+
+def run_sharded(mats, idx, devs, launch):
+    """One batched call per device over contiguous pieces of ``idx``: every piece is staged and
+    launched first (the devices run concurrently; launches are asynchronous), then each piece's
+    outputs are brought to the host. launch(store, device, offset) -> dict of device tensors
+    (None allowed); offset = the piece's position in ``idx`` (rsvd's global seed index).
+    Returns [(piece, {name: numpy or None})]. Results do not depend on the split (core.py:97-103)."""
+    pending = []
+    for k, (off, piece) in enumerate(split_contiguous(idx, len(devs))):
+        dev = devs[k]
+        with torch.cuda.device(dev):
+            store = stack_to_device(mats, piece, dev)
+            pending.append((piece, launch(store, dev, off)))
+    done = []
+    for piece, out in pending:
+        done.append((piece, {k: (None if v is None else to_host(v)) for k, v in out.items()}))
+    return done
+
+
 def stream_handle(device):
     return torch.cuda.current_stream(device).cuda_stream
 

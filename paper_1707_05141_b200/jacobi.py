@@ -22,6 +22,8 @@ from .core import (
     group_entries,
     ptr,
     resolve_device,
+    resolve_devices,
+    run_sharded,
     stack_to_device,
     stream_handle,
     to_host,
@@ -151,27 +153,28 @@ def svd_tensor(a, opts=None, *, rotations=False):
     )
 
 
-def batch_svd(batch, opts=None, *, threads=1, device=None):
-    """Per-entry :func:`svd` over a batch (jacobi.py:287-290); flags ride on each result."""
+def batch_svd(batch, opts=None, *, threads=1, device=None, devices=None):
+    """Per-entry :func:`svd` over a batch (jacobi.py:287-290); flags ride on each result.
+    ``devices``: shard the batch over several GPUs (contiguous pieces, one call per device)."""
     del threads
     opts = opts or JacobiOptions()
-    dev = resolve_device(device)
+    devs = resolve_devices(device, devices)
     groups, mats = group_entries(batch, _validate)
     out = [None] * len(mats)
     for (m, n, _), idx in groups.items():
-        store = stack_to_device(mats, idx, dev)
-        r = svd_colmajor(store, m, n, opts)
-        uh, sh = to_host(r["u"]), to_host(r["s"])
-        vh = to_host(r["v"]) if r["v"] is not None else None
-        swh, cvh = to_host(r["sweeps"]), to_host(r["converged"])
-        for j, i in enumerate(idx):
-            out[i] = SvdResult(
-                u=np.asfortranarray(uh[j].T),
-                sigma=sh[j].copy(),
-                v=None if vh is None else np.asfortranarray(vh[j].T),
-                converged=bool(cvh[j]),
-                sweeps=int(swh[j]),
-            )
+        def launch(store, dev, off):
+            r = svd_colmajor(store, m, n, opts)
+            return {"u": r["u"], "s": r["s"], "v": r["v"], "sweeps": r["sweeps"], "conv": r["converged"]}
+
+        for piece, h in run_sharded(mats, idx, devs, launch):
+            for j, i in enumerate(piece):
+                out[i] = SvdResult(
+                    u=np.asfortranarray(h["u"][j].T),
+                    sigma=h["s"][j].copy(),
+                    v=None if h["v"] is None else np.asfortranarray(h["v"][j].T),
+                    converged=bool(h["conv"][j]),
+                    sweeps=int(h["sweeps"][j]),
+                )
     return out
 
 

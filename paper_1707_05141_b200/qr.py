@@ -18,6 +18,8 @@ from .core import (
     group_entries,
     ptr,
     resolve_device,
+    resolve_devices,
+    run_sharded,
     stack_to_device,
     stream_handle,
     to_host,
@@ -69,18 +71,21 @@ def qr_tensor(a, panel_width=DEFAULT_PANEL_WIDTH):
     return from_colmajor(q), from_colmajor(r)
 
 
-def batch_qr(batch, panel_width=DEFAULT_PANEL_WIDTH, *, threads=1, device=None):
-    """Per-entry :func:`qr` over a batch (qr.py:98-100). ``threads`` is accepted and ignored."""
+def batch_qr(batch, panel_width=DEFAULT_PANEL_WIDTH, *, threads=1, device=None, devices=None):
+    """Per-entry :func:`qr` over a batch (qr.py:98-100). ``threads`` is accepted and ignored;
+    ``devices`` shards the batch over several GPUs."""
     del threads
-    dev = resolve_device(device)
+    devs = resolve_devices(device, devices)
     groups, mats = group_entries(batch, _validate(panel_width))
     out = [None] * len(mats)
     for (m, n, _), idx in groups.items():
-        store = stack_to_device(mats, idx, dev)
-        q, r = qr_colmajor(store, m, n, panel_width)
-        qh, rh = to_host(q), to_host(r)
-        for j, i in enumerate(idx):
-            out[i] = QrResult(q=np.asfortranarray(qh[j].T), r=np.asfortranarray(rh[j].T))
+        def launch(store, dev, off):
+            q, r = qr_colmajor(store, m, n, panel_width)
+            return {"q": q, "r": r}
+
+        for piece, h in run_sharded(mats, idx, devs, launch):
+            for j, i in enumerate(piece):
+                out[i] = QrResult(q=np.asfortranarray(h["q"][j].T), r=np.asfortranarray(h["r"][j].T))
     return out
 
 

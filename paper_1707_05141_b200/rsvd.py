@@ -20,6 +20,8 @@ from .core import (
     from_colmajor,
     ptr,
     resolve_device,
+    resolve_devices,
+    run_sharded,
     stream_handle,
     to_host,
     torch_dtype,
@@ -140,10 +142,12 @@ def rsvd_tensor(a, opts, *, index_base=0, omega=None):
     return dict(u=from_colmajor(r["u"]), s=r["s"], v=from_colmajor(r["v"]))
 
 
-def batch_rsvd(batch, opts, *, threads=1, device=None):
-    """Per-entry :func:`rsvd` with per-entry seeds ``opts.seed ^ index`` (rsvd.py:79-86)."""
+def batch_rsvd(batch, opts, *, threads=1, device=None, devices=None):
+    """Per-entry :func:`rsvd` with per-entry seeds ``opts.seed ^ index`` (rsvd.py:79-86).
+    ``devices`` shards the batch over several GPUs; every entry keeps its global index, so the
+    sketches (and results) do not depend on the split."""
     del threads
-    dev = resolve_device(device)
+    devs = resolve_devices(device, devices)
     entries = list(batch)
     mats, errors = [], {}
     for i, e in enumerate(entries):
@@ -165,15 +169,15 @@ def batch_rsvd(batch, opts, *, threads=1, device=None):
         while j + 1 < len(mats) and mats[j + 1].shape == mats[i].shape and mats[j + 1].dtype == mats[i].dtype:
             j += 1
         m, n = mats[i].shape
-        host = torch.empty((j - i + 1, n, m), dtype=torch_dtype(mats[i].dtype), pin_memory=True)
-        hv = host.numpy()
-        for t in range(i, j + 1):
-            hv[t - i] = mats[t].T
-        store = host.to(dev, non_blocking=True)
-        r = rsvd_colmajor(store, m, n, opts, index_base=i)
-        uh, sh, vh = to_host(r["u"]), to_host(r["s"]), to_host(r["v"])
-        for t in range(i, j + 1):
-            out[t] = TruncatedSvd(u=np.asfortranarray(uh[t - i].T), s=sh[t - i].copy(), v=np.asfortranarray(vh[t - i].T))
+        run0 = i
+
+        def launch(store, dev, off):
+            return rsvd_colmajor(store, m, n, opts, index_base=run0 + off)
+
+        for piece, h in run_sharded(mats, list(range(i, j + 1)), devs, launch):
+            for jj, t in enumerate(piece):
+                out[t] = TruncatedSvd(u=np.asfortranarray(h["u"][jj].T), s=h["s"][jj].copy(),
+                                      v=np.asfortranarray(h["v"][jj].T))
         i = j + 1
     return out
 

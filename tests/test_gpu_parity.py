@@ -538,3 +538,30 @@ def test_host_pipeline_matches_single_call():
     run_host_pipelined(lambda x, ib: [rsvd_colmajor(x, 24, 24, ro, index_base=ib)["s"]], host_in, outs, chunks=4,
                        index_base=3)
     assert torch.equal(outs[0], rref["s"].cpu())
+
+
+# ------------------------------------------------------------------ devices= sharding
+
+
+def test_devices_sharding_is_shard_invariant():
+    """devices= cuts each shape group into contiguous pieces, one batched call per device
+    (SURVEY §8b); the per-entry results are bitwise those of the single-device call (core.py:97-103),
+    including rsvd's seed ^ global index (rsvd.py:82-85). One GPU here: the same device twice."""
+    rng = np.random.default_rng(5)
+    mats = [rng.standard_normal((24, 16)) for _ in range(7)] + [rng.standard_normal((20, 20)) for _ in range(4)]
+    devs = ["cuda:0", "cuda:0", "cuda:0"]
+    for fn, kw in ((bf.batch_svd, dict(opts=bf.JacobiOptions(accumulate_v=True))), (bf.batch_qr, {}),
+                   (bf.batch_block_svd, dict(opts=bf.BlockJacobiOptions(block_width=4, accumulate_v=True))),
+                   (bf.batch_rsvd, dict(opts=bf.RsvdOptions(k=4, p=2, seed=77)))):
+        one = fn(mats, **kw)
+        many = fn(mats, devices=devs, **kw)
+        assert len(one) == len(many)
+        for x, y in zip(one, many):
+            for f in x.__dataclass_fields__:
+                a, b = getattr(x, f), getattr(y, f)
+                if isinstance(a, np.ndarray):
+                    assert np.array_equal(a, b), (fn.__name__, f)
+                else:
+                    assert a == b, (fn.__name__, f)
+    with pytest.raises(ValueError):
+        bf.batch_svd(mats, device="cuda:0", devices=devs)

@@ -98,3 +98,22 @@ def test_gloo_world2_shard_invariance(batch):
     np.testing.assert_array_equal(got["converged"], np.asarray(r["converged"]).astype(bool))
     rr = orc.batch_rsvd_stacked(a_rsvd, 24, 24, 4, 2, seed=7, index_base=0)
     np.testing.assert_array_equal(got["rsvd_s"], rr["s"])
+
+
+def test_bench_launcher_spawns_ranks_and_results_are_shard_invariant():
+    """`python bench.py --gpus 2` without torchrun re-launches itself under torch.distributed.run
+    with 2 ranks (the driver's form); --selftest runs the sharded path over gloo on CPU and checks
+    the gathered results against a single-rank run bit for bit."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--selftest"],
+                         capture_output=True, text=True, timeout=240, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["selftest"] == "ok" and line["world"] == 2 and line["backend"] == "gloo"
+    assert "torch.distributed.run" in line["launcher"]
+    for c in line["checks"].values():
+        assert c["bitwise_equal"] and len(c["shard_counts"]) == 2
