@@ -144,6 +144,35 @@ BF_API int bf_gemm_batched_f32(int64_t batch, int32_t M, int32_t N, int32_t K, c
                         int64_t a_stride, int32_t ta, const float* b, int32_t ldb, int64_t b_stride, int32_t tb,
                         float* c, int32_t ldc, int64_t c_stride, void* stream);
 
+/* ---- the reference's public helper functions, batched over independent entries (the drop-in
+ * calls them with batch = 1). All operands device pointers, column-major.
+ *   bf_householder_batched_*      replaces householder_vector  qr.py:26-48
+ *                                 (x, v: batch x len; tau: batch; v[0] = 1)
+ *   bf_jacobi_rotation_batched_f64 replaces jacobi_rotation   jacobi.py:68-80 (c, s per entry)
+ *   bf_off_orthogonality_batched_* replaces off_orthogonality jacobi.py:83-99 (a: m x n)
+ *   bf_scaled_offdiag_batched_*   replaces scaled_offdiag     blockjacobi.py:57-76 (g: n x n)
+ *   bf_syrk_batched_*             replaces syrk               core.py:68-78 (g = a^T a, mirrored)
+ *   bf_frobenius_batched_*        replaces frobenius          core.py:81-86
+ *   bf_axpby_*                    gemm's alpha/beta epilogue  core.py:36-65 (out = alpha p + beta c) */
+BF_API int bf_householder_batched_f64(int64_t batch, int32_t len, const double* x, double* v, double* tau,
+                               void* stream);
+BF_API int bf_householder_batched_f32(int64_t batch, int32_t len, const float* x, float* v, float* tau, void* stream);
+BF_API int bf_jacobi_rotation_batched_f64(int64_t batch, const double* g_pp, const double* g_pq, const double* g_qq,
+                                   double* c, double* s, void* stream);
+BF_API int bf_off_orthogonality_batched_f64(int64_t batch, int32_t m, int32_t n, const double* a, double* out,
+                                     void* stream);
+BF_API int bf_off_orthogonality_batched_f32(int64_t batch, int32_t m, int32_t n, const float* a, float* out,
+                                     void* stream);
+BF_API int bf_scaled_offdiag_batched_f64(int64_t batch, int32_t n, const double* g, double* out, void* stream);
+BF_API int bf_scaled_offdiag_batched_f32(int64_t batch, int32_t n, const float* g, float* out, void* stream);
+BF_API int bf_syrk_batched_f64(int64_t batch, int32_t m, int32_t k, const double* a, double* g, void* stream);
+BF_API int bf_syrk_batched_f32(int64_t batch, int32_t m, int32_t k, const float* a, float* g, void* stream);
+BF_API int bf_frobenius_batched_f64(int64_t batch, int32_t m, int32_t n, const double* a, double* out, void* stream);
+BF_API int bf_frobenius_batched_f32(int64_t batch, int32_t m, int32_t n, const float* a, float* out, void* stream);
+BF_API int bf_axpby_f64(int64_t n, double alpha, const double* p, double beta, const double* c, double* out,
+                 void* stream);
+BF_API int bf_axpby_f32(int64_t n, float alpha, const float* p, float beta, const float* c, float* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

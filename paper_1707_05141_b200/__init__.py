@@ -9,7 +9,17 @@ sm_100a CUDA kernels behind the C ABI in include/batchfact_b200.h
 
 from ._lib import BackendUnavailable
 from .blockjacobi import BlockJacobiOptions, BlockSvdResult, batch_block_svd, block_svd, block_svd_tensor
-from .core import BatchError, as_matrix
+from .core import BatchError, as_matrix, read_matrix_text, write_matrix_text
+from .helpers import (
+    batch_apply,
+    frobenius,
+    gemm,
+    householder_vector,
+    jacobi_rotation,
+    off_orthogonality,
+    scaled_offdiag,
+    syrk,
+)
 from .jacobi import (
     JacobiOptions,
     PairSchedule,
@@ -37,6 +47,16 @@ __all__ = [
     "SvdResult",
     "TruncatedSvd",
     "as_matrix",
+    "batch_apply",
+    "frobenius",
+    "gemm",
+    "householder_vector",
+    "jacobi_rotation",
+    "off_orthogonality",
+    "read_matrix_text",
+    "scaled_offdiag",
+    "syrk",
+    "write_matrix_text",
     "batch_block_svd",
     "batch_qr",
     "batch_rsvd",

@@ -68,6 +68,19 @@ EXPORTS = (
     "bf_rsvd_batched_f32",
     "bf_gaussian_batched_f64",
     "bf_gaussian_batched_f32",
+    "bf_householder_batched_f64",
+    "bf_householder_batched_f32",
+    "bf_jacobi_rotation_batched_f64",
+    "bf_off_orthogonality_batched_f64",
+    "bf_off_orthogonality_batched_f32",
+    "bf_scaled_offdiag_batched_f64",
+    "bf_scaled_offdiag_batched_f32",
+    "bf_syrk_batched_f64",
+    "bf_syrk_batched_f32",
+    "bf_frobenius_batched_f64",
+    "bf_frobenius_batched_f32",
+    "bf_axpby_f64",
+    "bf_axpby_f32",
     "bf_make_matrix_workspace_size",
     "bf_make_matrix_batched_f64",
 )
@@ -139,6 +152,19 @@ def load():
         f = getattr(L, name)
         f.argtypes = [I64, I32, I32, I32, P, I32, I64, I32, P, I32, I64, I32, P, I32, I64, P]
         f.restype = ctypes.c_int
+    F = ctypes.c_float
+    for suf, R in (("f64", D), ("f32", F)):
+        getattr(L, f"bf_householder_batched_{suf}").argtypes = [I64, I32, P, P, P, P]
+        getattr(L, f"bf_off_orthogonality_batched_{suf}").argtypes = [I64, I32, I32, P, P, P]
+        getattr(L, f"bf_scaled_offdiag_batched_{suf}").argtypes = [I64, I32, P, P, P]
+        getattr(L, f"bf_syrk_batched_{suf}").argtypes = [I64, I32, I32, P, P, P]
+        getattr(L, f"bf_frobenius_batched_{suf}").argtypes = [I64, I32, I32, P, P, P]
+        getattr(L, f"bf_axpby_{suf}").argtypes = [I64, R, P, R, P, P, P]
+        for nm in ("householder_batched", "off_orthogonality_batched", "scaled_offdiag_batched", "syrk_batched",
+                   "frobenius_batched", "axpby"):
+            getattr(L, f"bf_{nm}_{suf}").restype = ctypes.c_int
+    L.bf_jacobi_rotation_batched_f64.argtypes = [I64, P, P, P, P, P, P]
+    L.bf_jacobi_rotation_batched_f64.restype = ctypes.c_int
     _lib = L
     return L
 

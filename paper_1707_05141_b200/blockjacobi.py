@@ -13,6 +13,7 @@ from typing import Optional
 import numpy as np
 import torch
 
+from .helpers import scaled_offdiag  # noqa: F401  (reference re-exports, on the device)
 from . import _lib
 from .core import (
     check_batched_tensor,
@@ -98,7 +99,9 @@ def block_svd_colmajor(store, m, n, opts, *, stats=False):
     eh = torch.zeros((B, opts.max_sweeps), dtype=store.dtype, device=dev)
     sweeps = torch.empty(B, dtype=torch.int32, device=dev)
     conv = torch.empty(B, dtype=torch.uint8, device=dev)
-    ws, wsb = workspace(L.bf_block_svd_workspace_size(B, m, n, es, copts), dev)
+    with torch.cuda.device(dev):  # sizes depend on the device (occupancy, SM count)
+        nbytes = L.bf_block_svd_workspace_size(B, m, n, es, copts)
+    ws, wsb = workspace(nbytes, dev)
     st = torch.zeros((B, 4), dtype=torch.int64, device=dev) if stats else None
     fn = L.bf_block_svd_batched_ex_f64 if es == 8 else L.bf_block_svd_batched_ex_f32
     with torch.cuda.device(dev):

@@ -119,6 +119,8 @@ def _parser():
     c.add_argument("--error-vectors", type=int, default=30)
     c.add_argument("--report", default=None)
     c.add_argument("--device", default=None)
+    c.add_argument("--strict", action="store_true",
+                   help=f"exit {NONCONV_EXIT} when a batched Jacobi SVD of the truncation did not converge")
     return p
 
 
@@ -266,7 +268,8 @@ def main(argv=None):
         return 0
     try:
         if args.cmd == "compress":
-            rec, conv_all = _compress(args), True
+            rec = _compress(args)
+            conv_all = rec.get("nonconverged_entries", 0) == 0
         else:
             rec, conv_all = _bench(args)
     except ValueError as exc:

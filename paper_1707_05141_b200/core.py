@@ -49,6 +49,34 @@ def read_matrix_text(path, dtype=np.float64):
     return _r(path, dtype)
 
 
+def syrk(a, *, device=None):
+    """core.py:68-78 on the device (paper_1707_05141_b200.helpers)."""
+    from .helpers import syrk as _f
+
+    return _f(a, device=device)
+
+
+def gemm(a, b, c=None, *, alpha=1.0, beta=0.0, trans_a=False, trans_b=False, device=None):
+    """core.py:36-65 on the device (paper_1707_05141_b200.helpers)."""
+    from .helpers import gemm as _f
+
+    return _f(a, b, c, alpha=alpha, beta=beta, trans_a=trans_a, trans_b=trans_b, device=device)
+
+
+def frobenius(a, *, device=None):
+    """core.py:81-86 on the device (paper_1707_05141_b200.helpers)."""
+    from .helpers import frobenius as _f
+
+    return _f(a, device=device)
+
+
+def batch_apply(entries, op, *, threads=1):
+    """core.py:97-123 (paper_1707_05141_b200.helpers)."""
+    from .helpers import batch_apply as _f
+
+    return _f(entries, op, threads=threads)
+
+
 def resolve_device(device=None):
     if not torch.cuda.is_available():
         raise _lib.BackendUnavailable("no CUDA device visible; batchfact_b200 has no CPU fallback")

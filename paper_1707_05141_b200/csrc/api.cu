@@ -459,4 +459,41 @@ int bf_gemm_batched_f32(int64_t batch, int32_t M, int32_t N, int32_t K, const fl
   return gemm_impl<float>(batch, M, N, K, a, lda, as, ta, b, ldb, bs, tb, c, ldc, cs, st);
 }
 
+// ---------------------------------------------------------------- reference helpers
+#define BF_HELPER_PAIR(T, SUF)                                                                                   \
+  int bf_householder_batched_##SUF(int64_t batch, int32_t len, const T* x, T* v, T* tau, void* st) {             \
+    if (batch < 0 || len < 1) return fail(BF_ERR_ARG, "householder_vector expects a nonempty vector");            \
+    return cuda_rc(bf::launch_householder<T>(batch, len, x, v, tau, S(st)), "householder");                      \
+  }                                                                                                              \
+  int bf_off_orthogonality_batched_##SUF(int64_t batch, int32_t m, int32_t n, const T* a, T* out, void* st) {    \
+    if (batch < 0 || m < 0 || n < 0) return fail(BF_ERR_ARG, "negative batch or shape");                        \
+    return cuda_rc(bf::launch_offdiag<T>(batch, m, n, a, 1, out, S(st)), "off_orthogonality");                  \
+  }                                                                                                              \
+  int bf_scaled_offdiag_batched_##SUF(int64_t batch, int32_t n, const T* g, T* out, void* st) {                  \
+    if (batch < 0 || n < 0) return fail(BF_ERR_ARG, "negative batch or shape");                                 \
+    return cuda_rc(bf::launch_offdiag<T>(batch, n, n, g, 0, out, S(st)), "scaled_offdiag");                     \
+  }                                                                                                              \
+  int bf_syrk_batched_##SUF(int64_t batch, int32_t m, int32_t k, const T* a, T* g, void* st) {                   \
+    if (batch < 0 || m < 0 || k < 0) return fail(BF_ERR_ARG, "negative batch or shape");                        \
+    return cuda_rc(bf::launch_syrk<T>(batch, m, k, a, g, S(st)), "syrk");                                       \
+  }                                                                                                              \
+  int bf_frobenius_batched_##SUF(int64_t batch, int32_t m, int32_t n, const T* a, T* out, void* st) {            \
+    if (batch < 0 || m < 0 || n < 0) return fail(BF_ERR_ARG, "negative batch or shape");                        \
+    return cuda_rc(bf::launch_frobenius<T>(batch, (int64_t)m * n, a, out, S(st)), "frobenius");                 \
+  }                                                                                                              \
+  int bf_axpby_##SUF(int64_t n, T alpha, const T* p, T beta, const T* c, T* out, void* st) {                     \
+    if (n < 0) return fail(BF_ERR_ARG, "negative length");                                                       \
+    if (beta != T(0) && !c) return fail(BF_ERR_ARG, "beta != 0 requires c");                                     \
+    return cuda_rc(bf::launch_axpby<T>(n, alpha, p, beta, c, out, S(st)), "axpby");                             \
+  }
+BF_HELPER_PAIR(double, f64)
+BF_HELPER_PAIR(float, f32)
+#undef BF_HELPER_PAIR
+
+int bf_jacobi_rotation_batched_f64(int64_t batch, const double* gpp, const double* gpq, const double* gqq, double* c,
+                                   double* s, void* st) {
+  if (batch < 0) return fail(BF_ERR_ARG, "negative batch");
+  return cuda_rc(bf::launch_rotation(batch, gpp, gpq, gqq, c, s, S(st)), "jacobi_rotation");
+}
+
 }  // extern "C"

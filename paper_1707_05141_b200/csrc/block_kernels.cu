@@ -1116,10 +1116,10 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
   if (!bj_wide(kk)) {  // the one-CTA-per-pair step kernels (the wide pipeline needs no large smem)
     if (L.method == 0) {
       smem = (size_t)(2 * kk * kk + kk * 32 + 3 * kk) * sizeof(T) + (size_t)kk * sizeof(int) + 64;
-      e = cudaFuncSetAttribute(bj_gram_step<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      e = smem_optin((const void*)bj_gram_step<T>, (size_t)(smem));
     } else {
       smem = direct_smem<T>(L.m, kk, a.p_in_smem);
-      e = cudaFuncSetAttribute(bj_direct_step<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      e = smem_optin((const void*)bj_direct_step<T>, (size_t)(smem));
     }
     if (e != cudaSuccess) return (int)e;
   }
@@ -1175,12 +1175,12 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
     g.stats = L.stats;
     rot_smem = (size_t)2 * kk * (kk + 1) * sizeof(T);
     const int TT = kk / 16;
-    if (TT == 1) e = cudaFuncSetAttribute(bj_rot<T, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rot_smem);
-    if (TT == 2) e = cudaFuncSetAttribute(bj_rot<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rot_smem);
-    if (TT == 3) e = cudaFuncSetAttribute(bj_rot<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rot_smem);
-    if (TT == 4) e = cudaFuncSetAttribute(bj_rot<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rot_smem);
+    if (TT == 1) e = smem_optin((const void*)bj_rot<T, 1>, rot_smem);
+    if (TT == 2) e = smem_optin((const void*)bj_rot<T, 2>, rot_smem);
+    if (TT == 3) e = smem_optin((const void*)bj_rot<T, 3>, rot_smem);
+    if (TT == 4) e = smem_optin((const void*)bj_rot<T, 4>, rot_smem);
     if (e == cudaSuccess && kUseMma<T>(TT))
-      e = cudaFuncSetAttribute(bj_rot_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRotSmem);
+      e = smem_optin((const void*)bj_rot_mma, (size_t)(kRotSmem));
     if (e != cudaSuccess) return (int)e;
   }
   // batched direct pipeline (fp64, 2k = 64)
@@ -1237,11 +1237,10 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
     dqr_reg = L.m <= 256;
     dqr_smem = dqr_reg ? kDqrRegSmem : ((size_t)L.m * kk + kk + 2) * sizeof(double);
     dap_smem = kWySmem;
-    e = cudaFuncSetAttribute(dqr_reg ? bj_dqr_reg : bj_dqr, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)dqr_smem);
+    e = smem_optin((const void*)(dqr_reg ? bj_dqr_reg : bj_dqr), (size_t)(dqr_smem));
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(bj_dapply_wy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dap_smem);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(bj_rot_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRotSmem);
+      e = smem_optin((const void*)bj_dapply_wy, (size_t)(dap_smem));
+    if (e == cudaSuccess) e = smem_optin((const void*)bj_rot_mma, (size_t)(kRotSmem));
     if (e != cudaSuccess) return (int)e;
   }
   // wide pairs (2k > 64): staged pipeline over batched QR / GEMM / SVD launches
@@ -1373,7 +1372,7 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
   if (L.stats && (bg || bd || wide)) bj_stats_reduce<T><<<(unsigned)((L.batch + 255) / 256), 256, 0, st>>>(a);
   if ((e = cudaGetLastError()) != cudaSuccess) return (int)e;
   size_t xs = (size_t)np * (sizeof(T) + sizeof(int)) + 16;
-  e = cudaFuncSetAttribute(bj_extract<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)xs);
+  e = smem_optin((const void*)bj_extract<T>, (size_t)(xs));
   if (e != cudaSuccess) return (int)e;
   bj_extract<T><<<(unsigned)L.batch, 256, xs, st>>>(a, (T*)L.u, (T*)L.s, (T*)L.v, (T*)(base + lay.cand));
   return (int)cudaGetLastError();

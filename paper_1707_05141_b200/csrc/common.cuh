@@ -108,15 +108,6 @@ BF_DEV double unit_cos(double c0, double t) {
 // multiplied through by |den|, which leaves two independent reciprocal chains (t and c, s)
 // after h instead of four dependent ones. Exact IEEE fallback outside [1e-150, 1e150].
 BF_DEV void jacobi_rotation_t(double gpp, double gpq, double gqq, double& c, double& s, double& t) {
-#if defined(BF_EXP_ROT) && BF_EXP_ROT == 1
-  {  // experiment: the reference's formula with IEEE division / sqrt
-    const double zeta = (gqq - gpp) / (2.0 * gpq);
-    t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-    c = 1.0 / sqrt(fma(t, t, 1.0));
-    s = c * t;
-    return;
-  }
-#endif
   const double den = 2.0 * gpq, diff = gqq - gpp;
   const double aden = fabs(den), adiff = fabs(diff);
   const double big = aden > adiff ? aden : adiff;

@@ -57,6 +57,11 @@ struct GemmLaunch {
   int64_t c_stride;
 };
 
+// Opt a kernel into `need` bytes of dynamic shared memory. The attribute is process-wide state per
+// function and device, so concurrent host threads launching the same kernel with different sizes
+// must not lower it under each other: it is only ever raised (under a mutex).
+cudaError_t smem_optin(const void* func, size_t need);
+
 // all return 0 or a CUDA error code; dtype 0 = f64, 1 = f32
 size_t svd_global_ws_bytes(int dtype, int64_t batch, int m, int n, int ordering, bool accv, int tier, int max_sweeps);
 int launch_svd(int dtype, const SvdLaunch& L, void* ws, size_t ws_bytes, cudaStream_t st);
@@ -73,6 +78,20 @@ int launch_gaussian_f32(int64_t batch, int rows, int cols, uint64_t seed_lo, uin
                         int c_order = 0);
 int launch_sign_fix_f64(int64_t batch, int m, int n, double* q, const double* r, cudaStream_t st);
 int launch_scale_cols_f64(int64_t batch, int m, int n, double* q, const double* sigma, cudaStream_t st);
+
+// reference helper functions (helpers.cu)
+template <typename T>
+int launch_householder(int64_t batch, int len, const T* x, T* v, T* tau, cudaStream_t st);
+int launch_rotation(int64_t batch, const double* gpp, const double* gpq, const double* gqq, double* c, double* s,
+                    cudaStream_t st);
+template <typename T>
+int launch_offdiag(int64_t batch, int m, int n, const T* a, int gram, T* out, cudaStream_t st);
+template <typename T>
+int launch_syrk(int64_t batch, int m, int k, const T* a, T* g, cudaStream_t st);
+template <typename T>
+int launch_frobenius(int64_t batch, int64_t count, const T* a, T* out, cudaStream_t st);
+template <typename T>
+int launch_axpby(int64_t n, T alpha, const T* p, T beta, const T* c, T* out, cudaStream_t st);
 
 struct BlockLaunch {
   int64_t batch;

@@ -90,13 +90,8 @@ BF_DEV long long jacobi_step(T* W, int ldw, T* V, int ldv, int m, int nw, int or
         T* vq = V + (size_t)qq[j] * ldv;
         for (int i = lane; i < nw; i += 32) {
           T a = vp[i], b = vq[i];
-#if defined(BF_EXP_APPLY) && BF_EXP_APPLY == 1
-          vp[i] = c * a - s * b;  // experiment: numpy's op order, no contraction
-          vq[i] = s * a + c * b;
-#else
           vp[i] = fma(c, a, -s * b);
           vq[i] = fma(s, a, c * b);
-#endif
         }
       }
     }

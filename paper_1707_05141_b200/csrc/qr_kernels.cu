@@ -91,7 +91,7 @@ static int launch_qr_t(int64_t batch, int m, int n, const void* a, int64_t as, v
   p.gws_stride = (int64_t)((((size_t)m * n * sizeof(T) + 255) & ~(size_t)255) / sizeof(T));
   int nwarps = (n + 3) / 4;
   nwarps = nwarps < 2 ? 2 : (nwarps > BF_QRCTA_MAXW ? BF_QRCTA_MAXW : nwarps);
-  cudaError_t e = cudaFuncSetAttribute(qr_cta_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_optin((const void*)qr_cta_kernel<T>, (size_t)(smem));
   if (e != cudaSuccess) return (int)e;
   qr_cta_kernel<T><<<(unsigned)batch, nwarps * 32, smem, st>>>(p);
   return (int)cudaGetLastError();

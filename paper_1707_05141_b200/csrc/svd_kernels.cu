@@ -204,7 +204,7 @@ static int launch_svd_t(const SvdLaunch& L, void* ws, cudaStream_t st) {
   int pairs = a.nw / 2 > 0 ? a.nw / 2 : 1;
   int nwarps = (pairs + BF_CTA_PB - 1) / BF_CTA_PB;
   nwarps = nwarps < 2 ? 2 : (nwarps > BF_CTA_MAXW ? BF_CTA_MAXW : nwarps);
-  cudaError_t e = cudaFuncSetAttribute(svd_cta_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_optin((const void*)svd_cta_kernel<T>, (size_t)(smem));
   if (e != cudaSuccess) return (int)e;
   svd_cta_kernel<T><<<(unsigned)L.batch, nwarps * 32, smem, st>>>(a);
   return (int)cudaGetLastError();

@@ -217,8 +217,7 @@ static int launch_reg(const SvdLaunch& L, void* ws, size_t ws_bytes, cudaStream_
   const int nw = ORD == 1 ? C::np : L.n;
   const size_t smem = reg_smem_bytes<C>(L.m, nw, sizeof(T));
   if (smem > 227 * 1024) return -1;
-  cudaError_t e =
-      cudaFuncSetAttribute(svd_reg_kernel<T, C, ORD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_optin((const void*)svd_reg_kernel<T, C, ORD>, smem);
   if (e != cudaSuccess) return (int)e;
   int per_sm = 0, dev = 0, sms = 148;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, svd_reg_kernel<T, C, ORD>, C::threads, smem);

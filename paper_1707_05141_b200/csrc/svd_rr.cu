@@ -45,6 +45,8 @@ struct RRCfg {
 #define BF_RR_STAGE 8
 #endif
 constexpr int kRRStage = BF_RR_STAGE;
+// per-launch budget of the per-matrix rotation logs (the batch is chunked beyond it)
+constexpr size_t kRRLogBudget = (size_t)6 << 30;
 
 #ifndef BF_RR64_R
 #define BF_RR64_R 8  // rows per thread for 64 x 64 (8 -> 2 warps, 4 -> 4 warps per matrix)
@@ -55,8 +57,9 @@ struct RRShared {
   // carved out of the extraction work region (free during the sweeps)
   static constexpr int PART = 2 * C::NWARP * 2 * C::NPAIR;  // [parity][warp][2 * NPAIR]
   static constexpr int DN = C::NWARP * C::NP;               // tracked norms per warp
+  static constexpr int FS = C::NWARP * C::NP;               // column scales per warp
   static constexpr int STAGE = 2 * kRRStage * C::NPAIR * 2; // V log staging (doubles)
-  static constexpr int SWEEP = PART + DN;
+  static constexpr int SWEEP = PART + DN + FS;
 };
 
 BF_DEV void rr_bar(int nthreads) { asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory"); }
@@ -73,8 +76,7 @@ BF_DEV int rr_col(int x, int t) {
 template <class C>
 struct RRTile {
   static constexpr int S = C::S, R = C::R, SG = C::SG;
-  double A[R][S], B[R][S];  // physical FIFO registers (scaled columns: true = stored * scale)
-  double FA[S], FB[S];      // per-position column scales of this slot group (W phase)
+  double A[R][S], B[R][S];  // physical FIFO registers (W phase: scaled columns, true = stored * fs[col])
 
   // logical a[j] / b[j] at phase PH
   template <int PH>
@@ -101,31 +103,6 @@ struct RRTile {
         A[i][ia<PH>(j)] = fma(al[j], b, a);
         B[i][ib<PH>(j)] = fma(be[j], a, b);
       }
-  }
-  template <int PH>
-  BF_DEV void scale_update(const double (&c)[S]) {
-#pragma unroll
-    for (int j = 0; j < S; ++j) {
-      FA[ia<PH>(j)] *= c[j];
-      FB[ib<PH>(j)] *= c[j];
-    }
-  }
-  // fold the scales into the columns (phase independent: physical registers pair up)
-  BF_DEV void renormalize() {
-#pragma unroll
-    for (int x = 0; x < S; ++x) {
-#pragma unroll
-      for (int i = 0; i < R; ++i) {
-        A[i][x] *= FA[x];
-        B[i][x] *= FB[x];
-      }
-      FA[x] = 1.0;
-      FB[x] = 1.0;
-    }
-  }
-  BF_DEV void unit_scales() {
-#pragma unroll
-    for (int x = 0; x < S; ++x) FA[x] = FB[x] = 1.0;
   }
   // multiply columns by per-column factors (t == 0: position == column), phase PH
   template <int PH>
@@ -157,12 +134,11 @@ struct RRTile {
     // last slot group: the ring turns from position NP/2-1 to NP/2 inside the thread
     b[XB] = last ? a_exit : rb;
   }
-  template <int PH, bool SCALES>
+  template <int PH>
   BF_DEV void move(int sg) {
     const bool first = sg == 0, last = sg == SG - 1;
 #pragma unroll
     for (int i = 0; i < R; ++i) move1<PH>(A[i], B[i], first, last);
-    if (SCALES) move1<PH>(FA, FB, first, last);
   }
 
   template <int PH>
@@ -234,6 +210,7 @@ struct RRWork {
   double tol2;
   double* part;  // [2][NWARP][2 * NPAIR]
   double* d;     // this warp's NP tracked norms
+  double* fs;    // this warp's NP column scales (scaled rotations: true column = stored * fs[col])
   double2* log;  // global cursor (warp 0 writes): per step and slot (al, be)
   double* slog;  // global cursor (warp 0 writes): per sweep the NP column scales
   int ex, sweeps, conv, rot, recompute;
@@ -281,14 +258,10 @@ struct RRWork {
     cross_warp(v);
     if (rot_lane()) {
       const int k = slot();
-      double fa = tile.FA[RRTile<C>::template ia<PH>(0)], fb = tile.FB[RRTile<C>::template ib<PH>(0)];
-#pragma unroll
-      for (int j = 1; j < S; ++j) {
-        fa = rgl == j ? tile.FA[RRTile<C>::template ia<PH>(j)] : fa;
-        fb = rgl == j ? tile.FB[RRTile<C>::template ib<PH>(j)] : fb;
-      }
-      d[rr_col<NP>(k, t)] = v[0] * (fa * fa);
-      d[rr_col<NP>(NP - 1 - k, t)] = v[1] * (fb * fb);
+      const int ca = rr_col<NP>(k, t), cb = rr_col<NP>(NP - 1 - k, t);
+      const double fa = fs[ca], fb = fs[cb];
+      d[ca] = v[0] * (fa * fa);
+      d[cb] = v[1] * (fb * fb);
     }
     __syncwarp();
     recompute = 0;
@@ -308,22 +281,17 @@ struct RRWork {
     warp_sum(g);
     double v[1] = {pick<S>(g, rgl)};
     cross_warp(v);
-    double al = 0.0, be = 0.0, cc = 1.0;
+    double al = 0.0, be = 0.0;
     int flag = 0;
     if (rot_lane()) {
       const int k = slot();
-      double fa = tile.FA[RRTile<C>::template ia<PH>(0)], fb = tile.FB[RRTile<C>::template ib<PH>(0)];
-#pragma unroll
-      for (int j = 1; j < S; ++j) {
-        fa = rgl == j ? tile.FA[RRTile<C>::template ia<PH>(j)] : fa;
-        fb = rgl == j ? tile.FB[RRTile<C>::template ib<PH>(j)] : fb;
-      }
       const int ca = rr_col<NP>(k, t), cb = rr_col<NP>(NP - 1 - k, t);
+      const double fa = fs[ca], fb = fs[cb];
       const bool rev = ca > cb;  // slot a holds the larger column: rotate with swapped roles
       const int p = rev ? cb : ca, q = rev ? ca : cb;
       const double dpp = d[p], dqq = d[q], gpq = v[0] * (fa * fb);
       if (gpq * gpq > tol2 * (dpp * dqq)) {  // skip rule (jacobi.py:167)
-        double sn, tt;
+        double cc, sn, tt;
         jacobi_rotation_t(dpp, gpq, dqq, cc, sn, tt);
         const double np_ = dpp - tt * gpq, nq = dqq + tt * gpq;
         d[p] = np_ > 0.0 ? np_ : 0.0;
@@ -333,6 +301,8 @@ struct RRWork {
         const double rinv = rcp_fast(fa * fb);
         al = -tp * (fb * fb) * rinv;
         be = tp * (fa * fa) * rinv;
+        fs[ca] = fa * cc;  // the rotation's cosine moves into the column scales
+        fs[cb] = fb * cc;
         ++rot;
       }
       if (log != nullptr && warp == 0) log[k] = make_double2(al, be);
@@ -342,33 +312,31 @@ struct RRWork {
     // warps the next step's cross-warp barrier already does; racecheck-clean either way)
     if (NWARP == 1) __syncwarp();
     recompute = __any_sync(FULL, flag);
-    double a[S], b[S], c[S];
+    double a[S], b[S];
 #pragma unroll
     for (int j = 0; j < S; ++j) {
       a[j] = __shfl_sync(FULL, al, j * SG + sg);
       b[j] = __shfl_sync(FULL, be, j * SG + sg);
-      c[j] = __shfl_sync(FULL, cc, j * SG + sg);
     }
     tile.template apply<PH>(a, b);
-    tile.template scale_update<PH>(c);
-    tile.template move<PH, true>(sg);
+    tile.template move<PH>(sg);
   }
 
   // end of a sweep (t == 0 again: positions are columns): fold the scales into W, log them
   // for the V replay, and decide convergence
   template <int PH>
   BF_DEV bool sweep_end(RRTile<C>& tile) {
+    __syncwarp();  // this step's scale updates visible to the whole warp
     if (slog != nullptr) {
-      if (warp == 0 && rgl == 0) {
-#pragma unroll
-        for (int j = 0; j < S; ++j) {
-          slog[sg * S + j] = tile.FA[RRTile<C>::template ia<PH>(j)];
-          slog[NP - 1 - (sg * S + j)] = tile.FB[RRTile<C>::template ib<PH>(j)];
-        }
-      }
+      if (warp == 0)
+        for (int c = lane; c < NP; c += 32) slog[c] = fs[c];
       slog += NP;
     }
-    tile.renormalize();
+    // fold the scales into W (t == 0: positions are columns) and reset them
+    tile.template scale_cols<PH>(fs, sg);
+    __syncwarp();
+    for (int c = lane; c < NP; c += 32) fs[c] = 1.0;
+    __syncwarp();
     return sweep_end();
   }
 
@@ -430,7 +398,7 @@ struct RRReplay {
     }
     ++in_stage;
     tile.template apply<PH>(c, s);
-    tile.template move<PH, false>(sg);
+    tile.template move<PH>(sg);
   }
   BF_DEV bool sweep_end() { return --sweeps_left <= 0; }
 };
@@ -490,6 +458,7 @@ struct RRArgs {
   int64_t slog_stride;
   const uint8_t* active;
   int split_v;      // V replayed by svd_rr_vkernel: logs per matrix, vmeta written
+  int* queue;       // [0] W-kernel, [1] V-kernel work counters (zeroed before the launch) or null
   int32_t* vmeta;   // split_v: per matrix [replay sweeps, order[0..n)], stride nw + 1
 };
 
@@ -511,6 +480,17 @@ static size_t rr_smem_bytes(int m, int nw) {
 #ifndef BF_RR_MINB
 #define BF_RR_MINB 1
 #endif
+// Dynamic matrix queue: a CTA's first matrix is blockIdx.x, later ones are claimed from a global
+// counter, so CTAs that drew fast-converging matrices take more of them (sweep counts vary 7-11
+// per matrix; a static b += gridDim.x split left the last wave ragged). Block-uniform result.
+BF_DEV int64_t rr_claim(int* ctr, int64_t cur) {
+  __shared__ long long next;
+  __syncthreads();
+  if (threadIdx.x == 0) next = ctr ? (long long)gridDim.x + atomicAdd(ctr, 1) : cur + gridDim.x;
+  __syncthreads();
+  return next;
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::THREADS, BF_RR_MINB) svd_rr_kernel(RRArgs<double> a) {
   extern __shared__ __align__(16) double sm[];
@@ -525,11 +505,10 @@ __global__ void __launch_bounds__(C::THREADS, BF_RR_MINB) svd_rr_kernel(RRArgs<d
   const int row0 = (warp * C::RGW + rgl) * C::R;
   const bool accv = a.v != nullptr;
 
-  for (int64_t b = blockIdx.x; b < a.batch; b += gridDim.x) {
+  for (int64_t b = blockIdx.x; b < a.batch; b = rr_claim(a.queue, b)) {
     if (a.active && !a.active[b]) continue;  // uniform across the CTA
     const double* Ab = a.a + b * a.a_stride;
     RRTile<C> tile;
-    tile.unit_scales();
 #pragma unroll
     for (int j = 0; j < C::S; ++j) {
       const int ca = sg * C::S + j, cb = C::NP - 1 - (sg * C::S + j);
@@ -555,6 +534,7 @@ __global__ void __launch_bounds__(C::THREADS, BF_RR_MINB) svd_rr_kernel(RRArgs<d
     wk.tol2 = a.tol * a.tol;
     wk.part = Wsm;
     wk.d = Wsm + RRShared<C>::PART + warp * C::NP;
+    wk.fs = Wsm + RRShared<C>::PART + RRShared<C>::DN + warp * C::NP;
     const int64_t lslot = a.split_v ? b : (int64_t)blockIdx.x;
     wk.log = a.log ? a.log + lslot * a.log_stride : nullptr;
     wk.slog = a.log ? a.slog + lslot * a.slog_stride : nullptr;
@@ -565,6 +545,8 @@ __global__ void __launch_bounds__(C::THREADS, BF_RR_MINB) svd_rr_kernel(RRArgs<d
     wk.recompute = 0;
     wk.rots = 0;
     __syncthreads();  // previous matrix done with the shared region
+    for (int c = lane; c < C::NP; c += 32) wk.fs[c] = 1.0;
+    __syncwarp();
     int ph = 0;
     if (!wk.conv) ph = RRDriver<C, RRWork<C>>::run(tile, wk);
 
@@ -640,12 +622,11 @@ __global__ void __launch_bounds__(C::THREADS) svd_rr_vkernel(RRArgs<double> a) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int sg = lane % C::SG, rgl = lane / C::SG;
   const int row0 = (warp * C::RGW + rgl) * C::R;
-  for (int64_t b = blockIdx.x; b < a.batch; b += gridDim.x) {
+  for (int64_t b = blockIdx.x; b < a.batch; b = rr_claim(a.queue ? a.queue + 1 : nullptr, b)) {
     if (a.active && !a.active[b]) continue;
     const int32_t* vm = a.vmeta + b * (int64_t)(nw + 1);
     const int vs = vm[0];
     RRTile<C> tile;
-    tile.unit_scales();
 #pragma unroll
     for (int j = 0; j < C::S; ++j) {
       const int ca = sg * C::S + j, cb = C::NP - 1 - (sg * C::S + j);
@@ -684,7 +665,7 @@ template <class C>
 static int launch_rr(const SvdLaunch& L, int nw, void* ws, size_t ws_bytes, cudaStream_t st, size_t* need) {
   const size_t smem = rr_smem_bytes<C>(L.m, nw);
   if (smem > 227 * 1024) return -1;
-  cudaError_t e = cudaFuncSetAttribute(svd_rr_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = smem_optin((const void*)svd_rr_kernel<C>, (size_t)(smem));
   if (e != cudaSuccess) return (int)e;
   int per_sm = 0, dev = 0, sms = 148;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, svd_rr_kernel<C>, C::THREADS, smem);
@@ -692,59 +673,79 @@ static int launch_rr(const SvdLaunch& L, int nw, void* ws, size_t ws_bytes, cuda
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (per_sm < 1) per_sm = 1;
   const int64_t cap = (int64_t)per_sm * sms;
-  const int grid = (int)(L.batch < cap ? L.batch : cap);
   // the replay prefetches up to two stages past the last logged step
   const int64_t log_stride = ((int64_t)L.max_sweeps * (C::NP - 1) + 2 * kRRStage + 1) * C::NPAIR;
   const int64_t slog_stride = (int64_t)L.max_sweeps * C::NP;
   const bool split = L.v != nullptr;
-  const int64_t slots = split ? L.batch : grid;
-  const size_t log_bytes = L.v ? (size_t)slots * log_stride * sizeof(double2) + (size_t)slots * slog_stride * 8 +
-                                     (split ? (((size_t)L.batch * (nw + 1) * 4 + 255) & ~(size_t)255) : 0)
-                               : 0;
+  // With V the logs are per matrix (split_v). They are sized for max_sweeps, so the batch runs in
+  // chunks that keep the log workspace within kRRLogBudget (whole waves of CTAs per chunk);
+  // without V there is no log.
+  const size_t per_mat = (size_t)log_stride * sizeof(double2) + (size_t)slog_stride * 8 + (size_t)(nw + 1) * 4;
+  int64_t chunk = L.batch;
+  if (split) {
+    int64_t fit = (int64_t)(kRRLogBudget / per_mat);
+    fit = fit < cap ? cap : (fit / cap) * cap;
+    chunk = L.batch < fit ? L.batch : fit;
+  }
+  auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+  const size_t log_bytes = split ? al((size_t)chunk * log_stride * sizeof(double2)) +
+                                       al((size_t)chunk * slog_stride * 8) + al((size_t)chunk * (nw + 1) * 4)
+                                 : 0;
+  const size_t need_bytes = log_bytes + 256;  // + the work-queue counters
   if (need) {
-    *need = log_bytes;
+    *need = need_bytes;
     return 0;
   }
-  if (log_bytes && (!ws || ws_bytes < log_bytes)) return -2;
-  RRArgs<double> a;
-  a.batch = L.batch;
-  a.m = L.m;
-  a.n = L.n;
-  a.nw = nw;
-  a.a = (const double*)L.a;
-  a.a_stride = L.a_stride;
-  a.ta = L.transpose_a;
-  a.u = (double*)L.u;
-  a.u_stride = L.u_stride;
-  a.s = (double*)L.s;
-  a.s_stride = L.s_stride;
-  a.v = (double*)L.v;
-  a.v_stride = L.v_stride;
-  a.sweeps = L.sweeps;
-  a.conv = L.converged;
-  a.rots = L.rotations;
-  a.accum = L.accumulate;
-  a.tol = L.tol;
-  a.max_sweeps = L.max_sweeps;
-  a.log = L.v ? (double2*)ws : nullptr;
-  a.log_stride = log_stride;
-  a.slog = L.v ? (double*)((double2*)ws + (size_t)slots * log_stride) : nullptr;
-  a.slog_stride = slog_stride;
-  a.active = L.active;
-  a.split_v = split ? 1 : 0;
-  a.vmeta = split ? (int32_t*)(a.slog + (size_t)slots * slog_stride) : nullptr;
-  svd_rr_kernel<C><<<grid, C::THREADS, smem, st>>>(a);
-  if (!split) return (int)cudaGetLastError();
+  if (!ws || ws_bytes < need_bytes) return -2;
+  int* queue = (int*)((char*)ws + log_bytes);
   using CV = C;
   const size_t vsmem = ((size_t)RRShared<CV>::STAGE + (size_t)nw * nw) * 8;
-  e = cudaFuncSetAttribute(svd_rr_vkernel<CV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vsmem);
-  if (e != cudaSuccess) return (int)e;
-  int vper = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&vper, svd_rr_vkernel<CV>, CV::THREADS, vsmem);
-  if (vper < 1) vper = 1;
-  const int64_t vcap = (int64_t)vper * sms;
-  const int vgrid = (int)(L.batch < vcap ? L.batch : vcap);
-  svd_rr_vkernel<CV><<<vgrid, CV::THREADS, vsmem, st>>>(a);
+  int vgrid_cap = 0;
+  if (split) {
+    e = smem_optin((const void*)svd_rr_vkernel<CV>, (size_t)(vsmem));
+    if (e != cudaSuccess) return (int)e;
+    int vper = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&vper, svd_rr_vkernel<CV>, CV::THREADS, vsmem);
+    vgrid_cap = (vper < 1 ? 1 : vper) * sms;
+  }
+  for (int64_t c0 = 0; c0 < L.batch; c0 += chunk) {
+    const int64_t cb = L.batch - c0 < chunk ? L.batch - c0 : chunk;
+    RRArgs<double> a;
+    a.batch = cb;
+    a.m = L.m;
+    a.n = L.n;
+    a.nw = nw;
+    a.a = (const double*)L.a + c0 * L.a_stride;
+    a.a_stride = L.a_stride;
+    a.ta = L.transpose_a;
+    a.u = (double*)L.u + c0 * L.u_stride;
+    a.u_stride = L.u_stride;
+    a.s = (double*)L.s + c0 * L.s_stride;
+    a.s_stride = L.s_stride;
+    a.v = L.v ? (double*)L.v + c0 * L.v_stride : nullptr;
+    a.v_stride = L.v_stride;
+    a.sweeps = L.sweeps ? L.sweeps + c0 : nullptr;
+    a.conv = L.converged ? L.converged + c0 : nullptr;
+    a.rots = L.rotations ? L.rotations + c0 : nullptr;
+    a.accum = L.accumulate;
+    a.tol = L.tol;
+    a.max_sweeps = L.max_sweeps;
+    a.log = split ? (double2*)ws : nullptr;
+    a.log_stride = log_stride;
+    a.slog = split ? (double*)((char*)ws + al((size_t)chunk * log_stride * sizeof(double2))) : nullptr;
+    a.slog_stride = slog_stride;
+    a.active = L.active ? L.active + c0 : nullptr;
+    a.split_v = split ? 1 : 0;
+    a.vmeta = split ? (int32_t*)((char*)a.slog + al((size_t)chunk * slog_stride * 8)) : nullptr;
+    a.queue = queue;
+    cudaMemsetAsync(queue, 0, 2 * sizeof(int), st);
+    const int grid = (int)(cb < cap ? cb : cap);
+    svd_rr_kernel<C><<<grid, C::THREADS, smem, st>>>(a);
+    if (split) {
+      const int vgrid = (int)(cb < vgrid_cap ? cb : vgrid_cap);
+      svd_rr_vkernel<CV><<<vgrid, CV::THREADS, vsmem, st>>>(a);
+    }
+  }
   return (int)cudaGetLastError();
 }
 

@@ -1,4 +1,8 @@
 // Small batched helpers: tiled GEMM, numpy-compatible Gaussian sampler, column fixes.
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -190,7 +194,7 @@ __global__ void __launch_bounds__(256) gemm_mma_kernel(GemmLaunch g) {
 
 template <int NT, bool TA, bool TB>
 static void launch_gemm_mma_t(const GemmLaunch& g, cudaStream_t st) {
-  cudaFuncSetAttribute(gemm_mma_kernel<NT, TA, TB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGmSmem);
+  smem_optin((const void*)gemm_mma_kernel<NT, TA, TB>, kGmSmem);
   int dev = 0, sms = 148, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -542,6 +546,20 @@ int launch_scale_cols_f64(int64_t batch, int m, int n, double* q, const double* 
   if (batch == 0) return 0;
   scale_cols_kernel<<<(unsigned)batch, 256, 0, st>>>(batch, m, n, q, sigma);
   return (int)cudaGetLastError();
+}
+
+cudaError_t smem_optin(const void* func, size_t need) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> granted;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_pair(func, dev);
+  const auto it = granted.find(key);
+  if (it != granted.end() && it->second >= need) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need);
+  if (e == cudaSuccess) granted[key] = need;
+  return e;
 }
 
 }  // namespace bf

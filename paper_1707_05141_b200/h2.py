@@ -580,6 +580,16 @@ class SvdChoice:
     seed: int = 0
 
 
+# converged flags of the batched Jacobi factorisations inside one compress() call (None outside);
+# rsvd reports none (the reference drops the inner flag, rsvd.py:70-76)
+_CONV_TALLY = None
+
+
+def _tally(conv):
+    if _CONV_TALLY is not None:
+        _CONV_TALLY.append(conv)
+
+
 def _factor(A, choice, level, need_v=True):
     """Batched SVD of (B, M, N), M >= N: returns u (B, M, w), s (B, w) descending, v (B, N, w)
     (v is None for ``full`` when not ``need_v``: the Jacobi sweeps then skip V entirely).
@@ -605,6 +615,7 @@ def _factor(A, choice, level, need_v=True):
         Ap = torch.zeros(B, Mp, Np, dtype=A.dtype, device=A.device)
         Ap[:, :M, :N] = A
         r = block_svd_tensor(Ap, BlockJacobiOptions(block_width=bw, method="direct", accumulate_v=True))
+        _tally(r["converged"])
         # the padded columns are exactly zero: their sigma are 0 and sort last
         return r["u"][:, :M, :N], r["sigma"][:, :N], r["v"][:, :N, :N]
     if M > N and (N > 64 or M > 64):
@@ -614,8 +625,10 @@ def _factor(A, choice, level, need_v=True):
 
         q, rr = qr_tensor(A)
         r = svd_tensor(rr.contiguous(), JacobiOptions(ordering="round_robin", accumulate_v=need_v))
+        _tally(r["converged"])
         return bmm(q.contiguous(), r["u"].contiguous()), r["sigma"], r["v"]
     r = svd_tensor(A, JacobiOptions(ordering="round_robin", accumulate_v=need_v))
+    _tally(r["converged"])
     return r["u"], r["sigma"], r["v"]
 
 
@@ -778,9 +791,14 @@ def compress(H, eps=1e-7, svd=None, *, sync_timing=True):
         raise _lib.BackendUnavailable("compress runs on the GPU: move the H2Matrix with H.to('cuda')")
     _level_struct(H)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    global _CONV_TALLY
+    _CONV_TALLY = []
     t0 = time.perf_counter()
     ev[0].record()
-    newk, U, E, T, info = truncate_basis(H, eps, choice)
+    try:
+        newk, U, E, T, info = truncate_basis(H, eps, choice)
+    finally:
+        flags, _CONV_TALLY = _CONV_TALLY, None
     ev[1].record()
     cpl = project_coupling(H, T, newk)
     ev[2].record()
@@ -800,6 +818,8 @@ def compress(H, eps=1e-7, svd=None, *, sync_timing=True):
         truncation_ms=ev[0].elapsed_time(ev[1]) if sync_timing else None,
         projection_ms=ev[1].elapsed_time(ev[2]) if sync_timing else None,
         wall_s=wall,
+        svd_calls=len(flags),
+        nonconverged_entries=int(sum(int((~f.bool()).sum()) for f in flags)),
     )
     return Hc, report
 

@@ -14,6 +14,7 @@ from typing import Optional
 import numpy as np
 import torch
 
+from .helpers import jacobi_rotation, off_orthogonality  # noqa: F401  (reference re-exports, on the device)
 from . import _lib
 from .core import (
     check_batched_tensor,
@@ -123,7 +124,9 @@ def svd_colmajor(store, m, n, opts, *, rotations=False):
     sweeps = torch.empty(B, dtype=torch.int32, device=dev)
     conv = torch.empty(B, dtype=torch.uint8, device=dev)
     rots = torch.empty(B, dtype=torch.int64, device=dev) if rotations else None
-    ws, wsb = workspace(L.bf_svd_workspace_size(B, m, n, es, copts), dev)
+    with torch.cuda.device(dev):  # sizes depend on the device (occupancy, SM count)
+        nbytes = L.bf_svd_workspace_size(B, m, n, es, copts)
+    ws, wsb = workspace(nbytes, dev)
     fn = L.bf_svd_batched_f64 if es == 8 else L.bf_svd_batched_f32
     with torch.cuda.device(dev):
         rc = fn(B, m, n, ptr(store), ptr(u), ptr(s), ptr(v), ptr(sweeps), ptr(conv), ptr(rots), copts, ptr(ws), wsb,

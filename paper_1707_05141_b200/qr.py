@@ -10,6 +10,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
+from .helpers import householder_vector  # noqa: F401  (reference re-exports, on the device)
 from . import _lib
 from .core import (
     check_batched_tensor,
@@ -54,7 +55,9 @@ def qr_colmajor(store, m, n, panel_width=DEFAULT_PANEL_WIDTH):
     es = store.element_size()
     q = torch.empty((B, n, m), dtype=store.dtype, device=dev)
     r = torch.empty((B, n, n), dtype=store.dtype, device=dev)
-    ws, wsb = workspace(L.bf_qr_workspace_size(B, m, n, es), dev)
+    with torch.cuda.device(dev):  # sizes depend on the device (occupancy, SM count)
+        nbytes = L.bf_qr_workspace_size(B, m, n, es)
+    ws, wsb = workspace(nbytes, dev)
     fn = L.bf_qr_batched_f64 if es == 8 else L.bf_qr_batched_f32
     with torch.cuda.device(dev):
         rc = fn(B, m, n, ptr(store), ptr(q), ptr(r), int(panel_width), ptr(ws), wsb, stream_handle(dev))

@@ -107,7 +107,9 @@ def rsvd_colmajor(store, m, n, opts, *, index_base=0, omega_store=None):
     u = torch.empty((B, w, m), dtype=store.dtype, device=dev)
     s = torch.empty((B, w), dtype=store.dtype, device=dev)
     v = torch.empty((B, w, n), dtype=store.dtype, device=dev)
-    ws, wsb = workspace(L.bf_rsvd_workspace_size(B, m, n, opts.k, opts.p, es), dev)
+    with torch.cuda.device(dev):  # sizes depend on the device (occupancy, SM count)
+        nbytes = L.bf_rsvd_workspace_size(B, m, n, opts.k, opts.p, es)
+    ws, wsb = workspace(nbytes, dev)
     lo, hi = split_seed(opts.seed)
     fn = L.bf_rsvd_batched_f64 if es == 8 else L.bf_rsvd_batched_f32
     with torch.cuda.device(dev):

@@ -24,7 +24,9 @@ def make_matrix_tensor(batch, m, n, cond, rank=None, seed=0, *, mode="geometric"
     lo, hi = split_seed(seed)
     a = torch.empty((batch, n, m), dtype=torch.float64, device=dev)
     sig = torch.empty(n, dtype=torch.float64, device=dev)
-    ws, wsb = workspace(L.bf_make_matrix_workspace_size(batch, m, n), dev)
+    with torch.cuda.device(dev):  # sizes depend on the device (occupancy, SM count)
+        nbytes = L.bf_make_matrix_workspace_size(batch, m, n)
+    ws, wsb = workspace(nbytes, dev)
     with torch.cuda.device(dev):
         rc = L.bf_make_matrix_batched_f64(batch, m, n, _MODES.index(mode), float(cond), int(rank), lo, hi,
                                           int(index_base), ptr(a), ptr(sig), ptr(ws), wsb, stream_handle(dev))

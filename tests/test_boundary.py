@@ -93,3 +93,24 @@ def test_gemm_argument_errors_without_gpu():
     rc = L.bf_gemm_batched_f64(1, 4, 4, 4, None, 4, 16, 0, None, 4, 16, 0, None, 3, 16, None)
     assert rc == _lib.BF_ERR_ARG and "ldc" in _lib.last_error()
     assert L.bf_gemm_batched_f64(0, 4, 4, 4, None, 4, 16, 0, None, 4, 16, 0, None, 4, 16, None) == _lib.BF_OK
+
+
+def test_batch_apply_contract():
+    """batch_apply (core.py:97-123): per-entry results independent of threads, lowest failing
+    index raised as BatchError after the whole batch ran. Host orchestration, no GPU."""
+    import paper_1707_05141_b200 as bf
+
+    ran = []
+
+    def op(x):
+        ran.append(x)
+        if x in (3, 5):
+            raise ValueError(f"bad {x}")
+        return x * x
+
+    assert bf.batch_apply(range(4), lambda x: x + 1) == [1, 2, 3, 4]
+    assert bf.batch_apply(range(10), lambda x: x * 2, threads=4) == [2 * i for i in range(10)]
+    with pytest.raises(bf.BatchError) as ei:
+        bf.batch_apply(range(8), op, threads=3)
+    assert ei.value.index == 3 and isinstance(ei.value.cause, ValueError)
+    assert sorted(ran) == list(range(8))  # every entry still ran

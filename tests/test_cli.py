@@ -54,3 +54,17 @@ def test_bench_other_ops_and_strict(tmp_path):
     p = tmp_path / "g.txt"
     assert cli.main(["gen", "--m", "6", "--n", "4", "--seed", "3", "--out", str(p)]) == 0
     assert cli.read_matrix_text(p).shape == (6, 4)
+
+
+@pytest.mark.gpu
+def test_compress_strict_reports_convergence(tmp_path):
+    """compress carries the batched SVDs' converged flags: the JSON line counts the entries that
+    did not converge and --strict exits 2 when there are any (SPEC exit-code convention)."""
+    import json
+
+    rep = tmp_path / "c.jsonl"
+    rc = cli.main(["compress", "--n", "512", "--leaf-size", "32", "--cheb-order", "4", "--strict",
+                   "--report", str(rep), "--error-vectors", "4"])
+    line = json.loads(rep.read_text().splitlines()[-1])
+    assert line["svd_calls"] > 0 and line["nonconverged_entries"] == 0
+    assert rc == 0

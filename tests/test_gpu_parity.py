@@ -565,3 +565,57 @@ def test_devices_sharding_is_shard_invariant():
                     assert a == b, (fn.__name__, f)
     with pytest.raises(ValueError):
         bf.batch_svd(mats, device="cuda:0", devices=devs)
+
+
+# ------------------------------------------------------------------ reference helper re-exports
+
+
+def test_helper_reexports_vs_oracle():
+    """householder_vector, jacobi_rotation, off_orthogonality, scaled_offdiag, syrk, gemm and
+    frobenius (the names batchfact exports, __init__.py:3-23, + blockjacobi.scaled_offdiag) run on
+    the device and agree with the oracle's restatements / the reference's formulas."""
+    from paper_1707_05141_b200.blockjacobi import scaled_offdiag
+
+    rng = np.random.default_rng(3)
+    eps = np.finfo(np.float64).eps
+    for x in (rng.standard_normal(17), np.array([2.0]), np.array([3.0, 0.0, 0.0]), rng.standard_normal(64) * 1e-200):
+        v, tau = bf.householder_vector(x)
+        vo, to = orc.householder(x)
+        assert v.dtype == x.dtype and v[0] == 1.0
+        assert abs(tau - to) <= 4 * eps * max(abs(to), 1.0)
+        assert np.allclose(v, vo, rtol=8 * eps, atol=0)
+    v32, t32 = bf.householder_vector(rng.standard_normal(9).astype(np.float32))
+    assert v32.dtype == np.float32
+    with pytest.raises(ValueError):
+        bf.householder_vector(np.zeros((2, 2)))
+    for g in ((2.0, 0.5, 1.0), (1.0, 0.0, 3.0), (1.0, 1e-300, 1.0 + 1e-15), (5.0, -2.0, 5.0), (1e200, 1e199, 3e200)):
+        c, s = bf.jacobi_rotation(*g)
+        co, so = orc.rotation(*g)
+        assert abs(c - co) <= 2 * eps and abs(s - so) <= 2 * eps * max(abs(so), 1e-300)
+    a = rng.standard_normal((30, 12))
+    a[:, 3] = 0.0
+    assert abs(bf.off_orthogonality(a) - orc.off_orthogonality(a)) <= 64 * eps
+    assert bf.off_orthogonality(a[:, :1]) == 0.0
+    g = a.T @ a
+    assert abs(scaled_offdiag(g) - orc.scaled_offdiag(g)) <= 64 * eps
+    z = np.array([[0.0, 1.0], [1.0, 1.0]])
+    assert scaled_offdiag(z) == np.inf and bf.scaled_offdiag(np.zeros((2, 2))) == 0.0
+    with pytest.raises(ValueError):
+        scaled_offdiag(np.ones((2, 3)))
+    gs = bf.syrk(a)
+    assert np.array_equal(gs, gs.T) and np.allclose(gs, orc.syrk(a), rtol=0, atol=64 * eps * np.abs(gs).max())
+    b = rng.standard_normal((12, 7))
+    cc = rng.standard_normal((30, 7))
+    assert np.allclose(bf.gemm(a, b), a @ b, atol=1e-13)
+    assert np.allclose(bf.gemm(a, b, cc, alpha=2.0, beta=-0.5), 2.0 * (a @ b) - 0.5 * cc, atol=1e-13)
+    assert np.allclose(bf.gemm(b, a, trans_a=True, trans_b=True), b.T @ a.T, atol=1e-13)
+    nan_c = np.full((30, 7), np.nan)
+    assert np.all(np.isfinite(bf.gemm(a, b, nan_c, beta=0.0)))  # beta == 0 ignores c (core.py:37-40)
+    assert np.all(bf.gemm(a, b, alpha=0.0) == 0.0)
+    with pytest.raises(ValueError):
+        bf.gemm(a, a)
+    with pytest.raises(ValueError):
+        bf.gemm(a, b, beta=1.0)
+    assert abs(bf.frobenius(a) - np.linalg.norm(a)) <= 8 * eps * np.linalg.norm(a)
+    assert bf.frobenius(np.zeros((0, 3))) == 0.0
+    assert bf.frobenius(np.array([[1e300, 1e300]])) == pytest.approx(np.sqrt(2) * 1e300, rel=1e-15)
