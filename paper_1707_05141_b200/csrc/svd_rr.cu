@@ -22,6 +22,8 @@
 // of svd_reg.cu moves ~64 KB through shared memory per 64 x 64 step).
 // Column norms are tracked (dgesvj scheme, see jacobi_reg.cuh) and recomputed at sweep start
 // and after cancellation. V is rebuilt from a rotation log replayed on the same tiles.
+#include <cstdio>
+
 #include "internal.h"
 #include "jacobi_cta.cuh"
 #include "jacobi_reg.cuh"
@@ -215,6 +217,9 @@ struct RRWork {
   double* slog;  // global cursor (warp 0 writes): per sweep the NP column scales
   int ex, sweeps, conv, rot, recompute;
   long long rots;
+#ifdef BF_RR_PHASE
+  long long ph[6];
+#endif
 
   BF_DEV bool rot_lane() const { return rgl < S; }
   BF_DEV int slot() const { return sg * S + rgl; }
@@ -275,12 +280,21 @@ struct RRWork {
 
   template <int PH>
   BF_DEV void step(RRTile<C>& tile, int t) {
+#ifdef BF_RR_PHASE
+    long long c0 = clock64();
+#endif
     if (recompute) norms<PH>(tile, t);
     double g[S];
     tile.template partial_dots<PH>(g);
     warp_sum(g);
     double v[1] = {pick<S>(g, rgl)};
+#ifdef BF_RR_PHASE
+    long long c1 = clock64();
+#endif
     cross_warp(v);
+#ifdef BF_RR_PHASE
+    long long c2 = clock64();
+#endif
     double al = 0.0, be = 0.0;
     int flag = 0;
     if (rot_lane()) {
@@ -312,6 +326,9 @@ struct RRWork {
     // warps the next step's cross-warp barrier already does; racecheck-clean either way)
     if (NWARP == 1) __syncwarp();
     recompute = __any_sync(FULL, flag);
+#ifdef BF_RR_PHASE
+    long long c3 = clock64();
+#endif
     double a[S], b[S];
 #pragma unroll
     for (int j = 0; j < S; ++j) {
@@ -319,7 +336,19 @@ struct RRWork {
       b[j] = __shfl_sync(FULL, be, j * SG + sg);
     }
     tile.template apply<PH>(a, b);
+#ifdef BF_RR_PHASE
+    long long c4 = clock64();
+#endif
     tile.template move<PH>(sg);
+#ifdef BF_RR_PHASE
+    long long c5 = clock64();
+    ph[0] += c1 - c0;
+    ph[1] += c2 - c1;
+    ph[2] += c3 - c2;
+    ph[3] += c4 - c3;
+    ph[4] += c5 - c4;
+    ph[5] += 1;
+#endif
   }
 
   // end of a sweep (t == 0 again: positions are columns): fold the scales into W, log them
@@ -505,6 +534,9 @@ __global__ void __launch_bounds__(C::THREADS, BF_RR_MINB) svd_rr_kernel(RRArgs<d
   const int row0 = (warp * C::RGW + rgl) * C::R;
   const bool accv = a.v != nullptr;
 
+#ifdef BF_RR_PHASE
+  long long phs[6] = {0, 0, 0, 0, 0, 0};
+#endif
   for (int64_t b = blockIdx.x; b < a.batch; b = rr_claim(a.queue, b)) {
     if (a.active && !a.active[b]) continue;  // uniform across the CTA
     const double* Ab = a.a + b * a.a_stride;
@@ -544,11 +576,20 @@ __global__ void __launch_bounds__(C::THREADS, BF_RR_MINB) svd_rr_kernel(RRArgs<d
     wk.rot = 0;
     wk.recompute = 0;
     wk.rots = 0;
+#ifdef BF_RR_PHASE
+    if (b == blockIdx.x)
+      for (int i = 0; i < 6; ++i) wk.ph[i] = 0;
+    else
+      for (int i = 0; i < 6; ++i) wk.ph[i] = phs[i];
+#endif
     __syncthreads();  // previous matrix done with the shared region
     for (int c = lane; c < C::NP; c += 32) wk.fs[c] = 1.0;
     __syncwarp();
     int ph = 0;
     if (!wk.conv) ph = RRDriver<C, RRWork<C>>::run(tile, wk);
+#ifdef BF_RR_PHASE
+    for (int i = 0; i < 6; ++i) phs[i] = wk.ph[i];
+#endif
 
     // ---- W -> shared memory (column-major m x nw), off-orthogonality fallback, extraction
     __syncthreads();
@@ -607,6 +648,11 @@ __global__ void __launch_bounds__(C::THREADS, BF_RR_MINB) svd_rr_kernel(RRArgs<d
     }
     __syncthreads();
   }
+#ifdef BF_RR_PHASE
+  if (threadIdx.x == 0 && blockIdx.x < 4)
+    printf("rrphase blk %d steps %lld dots %lld xwarp %lld rot %lld apply %lld move %lld\n", blockIdx.x, phs[5], phs[0],
+           phs[1], phs[2], phs[3], phs[4]);
+#endif
 }
 
 // V replay as its own kernel (split_v): it needs no Gram or rotation state, so it runs at the
