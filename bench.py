@@ -60,10 +60,10 @@ def block_opts(c):
 
 
 def load_profile(name):
-    """Per-launch DRAM traffic of the config's dominant kernel from the committed ncu --set full
-    summary (profiles/ncu_full_r01.json, written by tools/ncu_summary.py)."""
+    """Per-launch DRAM traffic of the config's dominant kernel(s) from the committed ncu --set full
+    summary (profiles/ncu_full_r02.json, written by tools/ncu_summary.py)."""
     try:
-        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_full_r01.json")))
+        d = json.load(open(os.path.join(ROOT, "profiles", "ncu_full_r02.json")))
         return d.get(name, {})
     except Exception:  # noqa: BLE001
         return {}

@@ -705,6 +705,119 @@ __global__ void __launch_bounds__(C::THREADS) svd_rr_vkernel(RRArgs<double> a) {
   }
 }
 
+// V replay with FIXED columns: thread i holds row i of V (all NP columns in registers) and the
+// whole sweep's 63 (NP - 1) steps are unrolled, so each slot's column pair
+// (rr_col(k, t), rr_col(NP - 1 - k, t)) is a compile-time register pair. Nothing moves between
+// threads: a step is S coefficient loads (broadcast) and 2 FMAs per slot per thread -- no
+// shuffles and no FIFO selects (the tiled replay spent as many FSEL as DFMA on its moves).
+// Coefficients stream through shared memory in VST-step stages (VST divides NP - 1, so a stage
+// never straddles a sweep and every stage boundary is a compile-time step).
+template <int NP>
+struct VColCfg {
+  static constexpr int NPAIR = NP / 2, L = NP - 1;
+  static constexpr int THREADS = ((NP + 31) / 32) * 32;
+  static constexpr int pick(int d) { return d < 6 ? (L * NPAIR * 16 <= 20 * 1024 ? L : 1) : (L % d == 0 ? d : pick(d - 1)); }
+  static constexpr int VST = pick(16);  // steps per coefficient stage
+  static constexpr int STAGES = L / VST;
+};
+
+template <int NP>
+BF_DEV constexpr int vcol_col(int x, int t) {  // column held by position x at step t (rr_col)
+  return x == 0 ? 0 : 1 + ((x - 1 - t) % (NP - 1) + (NP - 1)) % (NP - 1);
+}
+
+template <int NP, int T0, int NS>
+BF_DEV void vcol_steps(double (&v)[NP], const double2* st) {
+  constexpr int NPAIR = NP / 2;
+#pragma unroll
+  for (int u = 0; u < NS; ++u) {
+    const int t = T0 + u;  // compile-time after unrolling
+#pragma unroll
+    for (int k = 0; k < NPAIR; ++k) {
+      const int ca = vcol_col<NP>(k, t), cb = vcol_col<NP>(NP - 1 - k, t);
+      const double2 e = st[u * NPAIR + k];  // (al, be) in position order (a = slot k, b = NP-1-k)
+      const double x = v[ca], y = v[cb];
+      v[ca] = fma(e.x, y, x);
+      v[cb] = fma(e.y, x, y);
+    }
+  }
+}
+
+template <int NP, int G>
+BF_DEV void vcol_sweep(double (&v)[NP], double2* stage, const double2*& log, int& cur) {
+  using C = VColCfg<NP>;
+  if constexpr (G < C::STAGES) {
+    // stage cur holds steps [G VST, (G + 1) VST); prefetch the next stage into cur ^ 1
+    cp_async_wait_all();
+    __syncthreads();
+    {
+      double2* dst = stage + (cur ^ 1) * C::VST * C::NPAIR;
+      for (int e = threadIdx.x; e < C::VST * C::NPAIR; e += C::THREADS) cp_async16(dst + e, log + e);
+      cp_async_commit();
+      log += C::VST * C::NPAIR;
+    }
+    vcol_steps<NP, G * C::VST, C::VST>(v, stage + cur * C::VST * C::NPAIR);
+    cur ^= 1;
+    vcol_sweep<NP, G + 1>(v, stage, log, cur);
+  }
+}
+
+// which widths replay V with fixed columns (measured, B200): 64 x 64 (cfg3) 7.83 -> 7.35 ms per
+// step; 40 x 40 (rsvd's inner SVD) is faster on the tiled replay (two thirds of its 64 threads
+// would hold no row)
+#ifndef BF_RR_VTILE
+template <int NP>
+constexpr bool kVCol = NP == 64;
+#else
+template <int NP>
+constexpr bool kVCol = false;
+#endif
+
+template <int NP>
+__global__ void __launch_bounds__(VColCfg<NP>::THREADS) svd_rr_vcol_kernel(RRArgs<double> a) {
+  using C = VColCfg<NP>;
+  extern __shared__ __align__(16) double smv[];
+  double2* stage = reinterpret_cast<double2*>(smv);      // 2 x VST x NPAIR
+  double* Vsm = smv + 2 * C::VST * C::NPAIR * 2;          // NP x NP (column-major) for the sorted write
+  const int n = a.n, nw = a.nw, row = threadIdx.x;
+  for (int64_t b = blockIdx.x; b < a.batch; b = rr_claim(a.queue ? a.queue + 1 : nullptr, b)) {
+    if (a.active && !a.active[b]) continue;
+    const int32_t* vm = a.vmeta + b * (int64_t)(nw + 1);
+    const int vs = vm[0];
+    double v[NP];
+#pragma unroll
+    for (int c = 0; c < NP; ++c) v[c] = (c == row) ? 1.0 : 0.0;
+    const double2* log = a.log + b * a.log_stride;
+    const double* slog = a.slog + b * a.slog_stride;
+    __syncthreads();  // previous matrix done with the stage / Vsm
+    if (vs > 0) {
+      // stage 0 of sweep 0
+      for (int e = threadIdx.x; e < C::VST * C::NPAIR; e += C::THREADS) cp_async16(stage + e, log + e);
+      cp_async_commit();
+      log += C::VST * C::NPAIR;
+      int cur = 0;
+      for (int sw = 0; sw < vs; ++sw) {
+        vcol_sweep<NP, 0>(v, stage, log, cur);
+        // sweep end: the W phase folded its column scales into W; apply them to V's columns
+#pragma unroll
+        for (int c = 0; c < NP; ++c) v[c] *= slog[c];
+        slog += NP;
+      }
+      cp_async_wait_all();
+    }
+    if (row < nw) {
+#pragma unroll
+      for (int c = 0; c < NP; ++c) Vsm[(size_t)c * nw + row] = v[c];
+    }
+    __syncthreads();
+    double* Vo = a.v + b * a.v_stride;
+    for (int e = threadIdx.x; e < n * n; e += C::THREADS) {
+      const int r = e / n, i = e % n;
+      Vo[(size_t)r * n + i] = Vsm[(size_t)vm[1 + r] * nw + i];
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------ dispatch
 
 template <class C>
@@ -754,6 +867,16 @@ static int launch_rr(const SvdLaunch& L, int nw, void* ws, size_t ws_bytes, cuda
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&vper, svd_rr_vkernel<CV>, CV::THREADS, vsmem);
     vgrid_cap = (vper < 1 ? 1 : vper) * sms;
   }
+  using VC = VColCfg<C::NP>;
+  const size_t vcol_smem = ((size_t)2 * VC::VST * VC::NPAIR * 2 + (size_t)C::NP * C::NP) * 8;
+  int vcol_cap = 0;
+  if (split && kVCol<C::NP>) {
+    e = smem_optin((const void*)svd_rr_vcol_kernel<C::NP>, vcol_smem);
+    if (e != cudaSuccess) return (int)e;
+    int vper = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&vper, svd_rr_vcol_kernel<C::NP>, VC::THREADS, vcol_smem);
+    vcol_cap = (vper < 1 ? 1 : vper) * sms;
+  }
   for (int64_t c0 = 0; c0 < L.batch; c0 += chunk) {
     const int64_t cb = L.batch - c0 < chunk ? L.batch - c0 : chunk;
     RRArgs<double> a;
@@ -788,8 +911,13 @@ static int launch_rr(const SvdLaunch& L, int nw, void* ws, size_t ws_bytes, cuda
     const int grid = (int)(cb < cap ? cb : cap);
     svd_rr_kernel<C><<<grid, C::THREADS, smem, st>>>(a);
     if (split) {
-      const int vgrid = (int)(cb < vgrid_cap ? cb : vgrid_cap);
-      svd_rr_vkernel<CV><<<vgrid, CV::THREADS, vsmem, st>>>(a);
+      if (kVCol<C::NP>) {
+        const int vgrid = (int)(cb < vcol_cap ? cb : vcol_cap);
+        svd_rr_vcol_kernel<C::NP><<<vgrid, VColCfg<C::NP>::THREADS, vcol_smem, st>>>(a);
+      } else {
+        const int vgrid = (int)(cb < vgrid_cap ? cb : vgrid_cap);
+        svd_rr_vkernel<CV><<<vgrid, CV::THREADS, vsmem, st>>>(a);
+      }
     }
   }
   return (int)cudaGetLastError();

@@ -40,10 +40,14 @@ STALL_PREFIX2 = "smsp__pcsamp_warps_issue_stalled_"
 
 # capture -> bench config whose dominant kernel it is (later entries win)
 CONFIG_OF = {"cfg1_svd_reg": "cfg1", "cfg2_qr_reg": "cfg2", "cfg3_svd_reg": "cfg3", "cfg4_svd_reg": "cfg4",
-             "cfg5_qr_reg": "cfg5", "cfg3_svd_rr": "cfg3", "cfg2_qr_reg2": "cfg2", "cfg4d_dqr_reg": "cfg4d"}
+             "cfg5_qr_reg": "cfg5", "cfg3_svd_rr": "cfg3", "cfg2_qr_reg2": "cfg2", "cfg4d_dqr_reg": "cfg4d",
+             "cfg4_svd_rr_inner": "cfg4", "cfg4d_bj_dqr_reg": "cfg4d", "cfg5_svd_rr_v": "cfg5"}
 
 
-CONFIG_SUM = {"cfg3": ["cfg3_svd_rr", "cfg3_svd_rr_v"]}
+# configs whose hot path is several kernels per step: the captured launches are summed
+CONFIG_SUM = {"cfg3": ["cfg3_svd_rr", "cfg3_svd_rr_v"],
+              "cfg4": ["cfg4_bj_gram_mma", "cfg4_svd_rr_inner", "cfg4_bj_rot_mma"],
+              "cfg4d": ["cfg4d_bj_dqr_reg", "cfg4d_bj_dapply_wy"]}
 
 
 def num(x):
@@ -106,7 +110,7 @@ def main(src, js, md):
             by_cfg[cfg] = {"kernel": r["kernel"],
                            "dram_bytes_per_launch": (r.get("dram_read", 0) + r.get("dram_write", 0)) or None,
                            "duration_ns_ncu": r.get("duration_ns"),
-                           "source": f"ncu --set full capture {name} (profiles/ncu_full_r01.md)"}
+                           "source": f"ncu --set full capture {name} ({os.path.basename(md)})"}
     # configs whose step launches several kernels: traffic = sum over the captured launches
     for cfg, parts in CONFIG_SUM.items():
         if all(p in res for p in parts):
@@ -114,7 +118,8 @@ def main(src, js, md):
                            "dram_bytes_per_launch": sum(res[p].get("dram_read", 0) + res[p].get("dram_write", 0)
                                                         for p in parts),
                            "duration_ns_ncu": sum(res[p].get("duration_ns", 0) for p in parts),
-                           "source": "ncu --set full captures " + ", ".join(parts) + " (profiles/ncu_full_r01.md)"}
+                           "source": "ncu --set full captures " + ", ".join(parts) + f" ({os.path.basename(md)}); "
+                                     "block configs: one launch of each kernel of a round-robin step"}
     json.dump({"captures": res, **by_cfg}, open(js, "w"), indent=1)
     lines = ["| capture | kernel | ncu dur (us) | DRAM R+W (MB) | DRAM % | FP64 pipe % | DMMA pipe % | occupancy % | regs | local ld/st sectors | top stalls |",
              "|---|---|---:|---:|---:|---:|---:|---:|---:|---|---|"]
