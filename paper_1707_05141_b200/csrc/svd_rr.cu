@@ -870,12 +870,14 @@ static int launch_rr(const SvdLaunch& L, int nw, void* ws, size_t ws_bytes, cuda
   using VC = VColCfg<C::NP>;
   const size_t vcol_smem = ((size_t)2 * VC::VST * VC::NPAIR * 2 + (size_t)C::NP * C::NP) * 8;
   int vcol_cap = 0;
-  if (split && kVCol<C::NP>) {
-    e = smem_optin((const void*)svd_rr_vcol_kernel<C::NP>, vcol_smem);
-    if (e != cudaSuccess) return (int)e;
-    int vper = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&vper, svd_rr_vcol_kernel<C::NP>, VC::THREADS, vcol_smem);
-    vcol_cap = (vper < 1 ? 1 : vper) * sms;
+  if constexpr (kVCol<C::NP>) {
+    if (split) {
+      e = smem_optin((const void*)svd_rr_vcol_kernel<C::NP>, vcol_smem);
+      if (e != cudaSuccess) return (int)e;
+      int vper = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&vper, svd_rr_vcol_kernel<C::NP>, VC::THREADS, vcol_smem);
+      vcol_cap = (vper < 1 ? 1 : vper) * sms;
+    }
   }
   for (int64_t c0 = 0; c0 < L.batch; c0 += chunk) {
     const int64_t cb = L.batch - c0 < chunk ? L.batch - c0 : chunk;
@@ -911,7 +913,7 @@ static int launch_rr(const SvdLaunch& L, int nw, void* ws, size_t ws_bytes, cuda
     const int grid = (int)(cb < cap ? cb : cap);
     svd_rr_kernel<C><<<grid, C::THREADS, smem, st>>>(a);
     if (split) {
-      if (kVCol<C::NP>) {
+      if constexpr (kVCol<C::NP>) {
         const int vgrid = (int)(cb < vcol_cap ? cb : vcol_cap);
         svd_rr_vcol_kernel<C::NP><<<vgrid, VColCfg<C::NP>::THREADS, vcol_smem, st>>>(a);
       } else {
