@@ -743,11 +743,28 @@ BF_DEV void vcol_steps(double (&v)[NP], const double2* st) {
   }
 }
 
-template <int NP, int G>
+// positions 1..NP-1 advance D places: new[x] = old[1 + (x - 1 - D) mod (NP - 1)] -- the data
+// returns to "position order at the current step" so the next block reuses the same code
+template <int NP, int D>
+BF_DEV void vcol_rotate(double (&v)[NP]) {
+  double tmp[NP];
+#pragma unroll
+  for (int x = 1; x < NP; ++x) tmp[x] = v[x];
+#pragma unroll
+  for (int x = 1; x < NP; ++x) v[x] = tmp[1 + ((x - 1 - D) % (NP - 1) + (NP - 1)) % (NP - 1)];
+}
+
+// One sweep: STAGES blocks of VST steps. Registers hold V's row in POSITION order as of the
+// block's first step, so every block runs the same VST-step code (compile-time register pairs
+// of steps 0..VST-1) followed by an in-register rotation by VST positions (NP - 1 moves per
+// block instead of a 63-step unrolled body that thrashed the instruction cache: ncu
+// no_instructions 41-52 %). After a sweep the ring is back at position == column.
+template <int NP>
 BF_DEV void vcol_sweep(double (&v)[NP], double2* stage, const double2*& log, int& cur) {
   using C = VColCfg<NP>;
-  if constexpr (G < C::STAGES) {
-    // stage cur holds steps [G VST, (G + 1) VST); prefetch the next stage into cur ^ 1
+#pragma unroll 1
+  for (int g = 0; g < C::STAGES; ++g) {
+    // stage cur holds this block's coefficients; prefetch the next block into cur ^ 1
     cp_async_wait_all();
     __syncthreads();
     {
@@ -756,9 +773,9 @@ BF_DEV void vcol_sweep(double (&v)[NP], double2* stage, const double2*& log, int
       cp_async_commit();
       log += C::VST * C::NPAIR;
     }
-    vcol_steps<NP, G * C::VST, C::VST>(v, stage + cur * C::VST * C::NPAIR);
+    vcol_steps<NP, 0, C::VST>(v, stage + cur * C::VST * C::NPAIR);
+    vcol_rotate<NP, C::VST>(v);
     cur ^= 1;
-    vcol_sweep<NP, G + 1>(v, stage, log, cur);
   }
 }
 
@@ -797,7 +814,7 @@ __global__ void __launch_bounds__(VColCfg<NP>::THREADS) svd_rr_vcol_kernel(RRArg
       log += C::VST * C::NPAIR;
       int cur = 0;
       for (int sw = 0; sw < vs; ++sw) {
-        vcol_sweep<NP, 0>(v, stage, log, cur);
+        vcol_sweep<NP>(v, stage, log, cur);
         // sweep end: the W phase folded its column scales into W; apply them to V's columns
 #pragma unroll
         for (int c = 0; c < NP; ++c) v[c] *= slog[c];
