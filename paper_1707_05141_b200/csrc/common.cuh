@@ -31,14 +31,10 @@ BF_DEV T warp_allreduce_max(T v) {
   return v;
 }
 
-// Fast reciprocal / reciprocal square root: MUFU seed, one third-order correction, one Newton
-// step (~1 ulp, UNBIASED). The MUFU f64 seeds are coarse (~2^-14 relative); two plain Newton
-// steps from them leave a systematic -1.5 e1^2 error (Newton for rsqrt / rcp converges from
-// below) of ~0.2 ulp, which the Jacobi rotations turned into a steady shrink of the V columns
-// (mean ||v_j||^2 - 1 of -1.9e-15 vs the oracle's +2.6e-16 at 64 x 64, growing linearly through
-// the block method's V_R products). The cubic first step leaves e1 ~ e0^3, so the final Newton
-// step's quadratic term is far below an ulp and only round-to-nearest errors remain.
-// Only used on arguments in the normal range (callers fall back otherwise).
+// Fast reciprocal / reciprocal square root: MUFU seed, one third-order correction and one Newton
+// step (<= ~1 ulp; the final step's quadratic error term is far below an ulp, so only the
+// round-to-nearest errors of the last operations remain). Only used on arguments in the normal
+// range (callers fall back otherwise).
 BF_DEV double rcp_fast(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));

@@ -218,11 +218,14 @@ struct QrReg {
 #ifndef BF_QR40_G
 #define BF_QR40_G 1  // measured: G = 2 is slower for 128x40 (1.98 vs 1.93 ms)
 #endif
+#ifndef BF_QR_MINB
+#define BF_QR_MINB 1
+#endif
 #ifndef BF_QR_G
 #define BF_QR_G 4  // measured: 64x32 x10000 0.590 -> 0.571 ms (G = 2: 0.580)
 #endif
 template <int N, int R, int WW, int G = 1>
-__global__ void __launch_bounds__(WW * 32 * G) qr_reg_kernel(int64_t batch, int m, const double* A, int64_t as,
+__global__ void __launch_bounds__(WW * 32 * G, BF_QR_MINB) qr_reg_kernel(int64_t batch, int m, const double* A, int64_t as,
                                                              double* Q, int64_t qs, double* Rout, int64_t rs) {
   static_assert(G * WW <= 15, "one named barrier per matrix group");
   __shared__ double tb_all[G][WW * 32 * QrReg<N, R, WW>::TSN];

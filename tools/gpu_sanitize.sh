@@ -4,4 +4,3 @@ for tool in racecheck memcheck synccheck; do
   tail -3 gpurun_out/sanitize_$tool.log
 done
 timeout 600 python -m pytest tests -m gpu -x -q -p no:cacheprovider -k "svd or rsvd" 2>&1 | tail -1
-python tools/time_variants.py 2>&1 | grep "tier=auto" | grep "40x40"

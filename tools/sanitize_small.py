@@ -26,6 +26,28 @@ b = bf.block_svd_tensor(bf.gaussian_tensor(2, 128, 128, 11, seed_mode="add"),
                         bf.BlockJacobiOptions(method="direct", block_width=32, accumulate_v=True))
 r3 = bf.svd_tensor(bf.gaussian_tensor(2, 128, 122, 12, seed_mode="add"),
                    bf.JacobiOptions(ordering="round_robin", accumulate_v=True))  # CTA tier, V in global
+# round 2: the fixed-column V replay (64 wide, also inside the direct block method), the float32
+# Gaussian stream and f32 rsvd with a device sketch, the wide-pair block pipeline (2k > 64) with
+# work counters, the helper re-exports, devices= sharding
+QUICK = bool(os.environ.get("BF_SANITIZE_QUICK"))  # racecheck: small batches, no H^2
+r64 = bf.svd_tensor(bf.gaussian_tensor(8 if QUICK else 700, 64, 64, 13, seed_mode="add"), bf.JacobiOptions(ordering="round_robin",
+                                                                                           accumulate_v=True))
+g32 = bf.gaussian_tensor(5, 130, 41, 14, dtype=torch.float32)
+t32 = bf.rsvd_tensor(bf.gaussian_tensor(4, 64, 48, 15).float(), bf.RsvdOptions(k=8, p=4, seed=3))
+for meth in ("gram", "direct"):
+    bw = bf.block_svd_tensor(bf.gaussian_tensor(2, 130, 100, 16, seed_mode="add"),
+                             bf.BlockJacobiOptions(method=meth, block_width=48, accumulate_v=True), stats=True)
+x = np.random.default_rng(0).standard_normal((20, 9))
+bf.householder_vector(x[:, 0]), bf.jacobi_rotation(2.0, 0.5, 1.0), bf.off_orthogonality(x), bf.syrk(x)
+bf.gemm(x, x.T, np.ones((20, 20)), alpha=2.0, beta=0.5), bf.frobenius(x)
+from paper_1707_05141_b200.blockjacobi import scaled_offdiag  # noqa: E402
+
+scaled_offdiag(x.T @ x)
+bf.batch_svd([x, x[:, :5], x], devices=["cuda:0", "cuda:0"])
+if QUICK:
+    torch.cuda.synchronize()
+    print("sanitize workload ok (quick)")
+    sys.exit(0)
 from paper_1707_05141_b200 import h2  # noqa: E402
 
 g = h2.bmm(torch.randn(3, 30, 17, device=dev, dtype=torch.float64), torch.randn(3, 17, 64, device=dev, dtype=torch.float64))
