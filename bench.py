@@ -487,13 +487,17 @@ def measure(name, cfg, device, rank, world, args, flush, peaks, barrier, max_ove
     ent["kernels_per_step"] = dict(kinds)
     if e2e:
         e2e_steps = max(3, min(steps, 5))
-        t_e2e, h2d, d2h = time_e2e(gc, e2e_steps, args.e2e_chunks)
+        # host-buffer pipeline depth: enough chunks to overlap the PCIe copies with compute, but each
+        # chunk must stay a full-GPU call (the small and block configs are latency / wave bound:
+        # 12 chunks of cfg1 or cfg4 would each run at one matrix's latency)
+        chunks = args.e2e_chunks if args.e2e_chunks != 0 else -E2E_CHUNKS.get(name, 12)
+        t_e2e, h2d, d2h = time_e2e(gc, e2e_steps, chunks)
         t_e2e = max_over_ranks(t_e2e)
         ent["e2e"] = {"value": gc.global_batch * e2e_steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
                       "d2h_bytes_per_step": d2h,
                       "path": "host-buffer call (paper_1707_05141_b200.stream.run_host_pipelined: one C-ABI batched "
                               "call per chunk) with pinned HOST buffers: H2D of A, D2H of every output inside the "
-                              "timed region", "chunks": args.e2e_chunks}
+                              "timed region", "chunks": abs(chunks)}
     if dropin:
         dsteps = 2
         t_d = max_over_ranks(time_dropin(gc, dsteps))
@@ -504,6 +508,9 @@ def measure(name, cfg, device, rank, world, args, flush, peaks, barrier, max_ove
     torch.cuda.empty_cache()
     return ent
 
+
+# per-config e2e pipeline chunks (default; --e2e-chunks overrides)
+E2E_CHUNKS = {"cfg1": 2, "cfg2": 12, "cfg3": 12, "cfg4": 2, "cfg4d": 2, "cfg5": 8}
 
 BATCH_SWEEP = [125, 250, 500, 1000, 2000, 4000, 8000, 16000]
 
@@ -564,7 +571,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-dropin", action="store_true", help="skip the list-in drop-in e2e leg")
     ap.add_argument("--batch-sweep", action="store_true", help="also time the headline config at several batch sizes")
-    ap.add_argument("--e2e-chunks", type=int, default=-12,
+    ap.add_argument("--e2e-chunks", type=int, default=0,
                     help="host-buffer pipeline chunks for the e2e leg (negative: equal chunks, no taper)")
     ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
                     help="weak: every rank runs the config's full batch; strong: the config's batch is split "
