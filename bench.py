@@ -625,8 +625,15 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        # BF_BENCH_SHARE_GPU=1 (functional check of the multi-rank path on a one-GPU box): ranks
+        # share the visible GPUs round-robin and talk over gloo (NCCL refuses two ranks per GPU);
+        # timings from such a run are not scaling numbers
+        if os.environ.get("BF_BENCH_SHARE_GPU"):
+            local = local % torch.cuda.device_count()
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl")
     device = torch.device("cuda", local)
     torch.cuda.set_device(device)
     peaks = load_peaks()
@@ -640,7 +647,7 @@ def main():
     def max_over_ranks(x):
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=device)
+        t = torch.tensor([x], dtype=torch.float64, device=device if dist.get_backend() == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
