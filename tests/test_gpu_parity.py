@@ -619,3 +619,16 @@ def test_helper_reexports_vs_oracle():
     assert abs(bf.frobenius(a) - np.linalg.norm(a)) <= 8 * eps * np.linalg.norm(a)
     assert bf.frobenius(np.zeros((0, 3))) == 0.0
     assert bf.frobenius(np.array([[1e300, 1e300]])) == pytest.approx(np.sqrt(2) * 1e300, rel=1e-15)
+
+
+def test_rr_log_chunking_is_invisible():
+    """With V the round-robin tier logs rotations per matrix, sized for max_sweeps; a call whose
+    logs exceed the per-launch budget (svd_rr.cu kRRLogBudget) runs in chunks of whole CTA waves.
+    max_sweeps = 300 forces 3 chunks for 1 300 64x64 matrices; every matrix converges far below 30
+    sweeps, so the result must equal the unchunked max_sweeps = 30 call bit for bit."""
+    a = dev_gauss(1300, 64, 64, 3_100_000)
+    r30 = bf.svd_tensor(a, bf.JacobiOptions(ordering="round_robin", accumulate_v=True, max_sweeps=30))
+    r300 = bf.svd_tensor(a, bf.JacobiOptions(ordering="round_robin", accumulate_v=True, max_sweeps=300))
+    assert bool(torch.all(r30["converged"])) and int(r30["sweeps"].max()) < 30
+    for k in ("u", "sigma", "v", "sweeps", "converged"):
+        assert torch.equal(r30[k], r300[k]), k
