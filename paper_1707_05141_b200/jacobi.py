@@ -22,12 +22,9 @@ from .core import (
     from_colmajor,
     group_entries,
     ptr,
-    resolve_device,
     resolve_devices,
     run_sharded,
-    stack_to_device,
     stream_handle,
-    to_host,
     workspace,
 )
 
