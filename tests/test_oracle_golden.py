@@ -198,3 +198,29 @@ def test_rsvd_matches_reference(nm):
     k = int(c["k"])
     assert vec_mismatch(r["u"][:, :k], c["u"][:, :k], c["s"][:k], a.dtype, factor=4096.0) <= 1.0
     assert vec_mismatch(r["v"][:, :k], c["v"][:, :k], c["s"][:k], a.dtype, factor=4096.0) <= 1.0
+
+
+@pytest.mark.parametrize("name,m,seed,ordering,count", [("cfg1f32", 32, 1_000_000, "serial", 300),
+                                                        ("cfg1rrf32", 32, 1_000_000, "round_robin", 300),
+                                                        ("cfg3f32", 64, 3_000_000, "round_robin", 100)])
+def test_f32_oracle_vs_reference_stats(name, m, seed, ordering, count):
+    """float32: the oracle against the reference's own per-entry results on the cfg*f32 inputs
+    (tests/golden/ref_f32_stats.npz, tools/ref_runs/f32_ref.py): flags equal, sweeps within +-2
+    (float32 converges at its rounding noise floor), residual distributions matching the
+    reference's (medians within 3 %, maxima within 10 % on these subsets)."""
+    z = golden("ref_f32_stats")
+    idx = z[f"{name}/index"][:count]
+    a3 = np.stack([np.ascontiguousarray(orc.gaussian_matrix(m, m, seed + int(i), np.float32).T) for i in idx])
+    o = orc.batch_svd_stacked(a3, m, m, ordering=ordering, accumulate_v=True, threads=4)
+    assert np.array_equal(o["converged"], z[f"{name}/converged"][:count])
+    d = o["sweeps"] - z[f"{name}/sweeps"][:count]
+    assert np.max(np.abs(d)) <= 2 and np.mean(d == 0) > 0.8
+    u = o["u"].transpose(0, 2, 1).astype(np.float64)
+    v = o["v"].transpose(0, 2, 1).astype(np.float64)
+    eye = np.eye(m)
+    ou = np.sqrt(np.sum((np.matmul(u.transpose(0, 2, 1), u) - eye) ** 2, axis=(1, 2)))
+    ov = np.sqrt(np.sum((np.matmul(v.transpose(0, 2, 1), v) - eye) ** 2, axis=(1, 2)))
+    for mine, key in ((ou, "orth_u"), (ov, "orth_v")):
+        ref = z[f"{name}/{key}"][:count]
+        assert abs(np.median(mine) / np.median(ref) - 1) < 0.03, key
+        assert mine.max() <= 1.10 * ref.max(), key

@@ -1,8 +1,9 @@
 """Full-config parity on the GPU: EVERY entry of cfg1 (both orderings), cfg2, cfg3, cfg4 (Gram),
-cfg4d (direct) and cfg5 through the CUDA path against the CPU oracle on the same inputs
-(tools/parity_full.py: sigma normwise <= 1e-12, U/V equal up to sign, converged/sweeps rules,
-residual maxima no worse than the oracle's own maxima on the batch). The committed record of a
-run is profiles/parity_r02.json."""
+cfg4d (direct) and cfg5, and their float32 twins, through the CUDA path against the CPU oracle on
+the same inputs (tools/parity_full.py: sigma normwise <= 1e-12 / 1e-5, U/V equal up to sign,
+converged/sweeps rules, residual maxima no worse than the oracle's -- and for float32 the
+reference's own -- maxima on the batch). Committed records: profiles/parity_r02.json,
+profiles/parity_f32_r02.json."""
 
 import os
 import sys

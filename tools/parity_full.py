@@ -3,6 +3,8 @@ the CPU oracle (oracle/: the reference algorithm restated in C, pinned to the re
 outputs by tests/golden) on the same inputs.
 
     python tools/parity_full.py [--configs cfg1,cfg1rr,cfg2,cfg3,cfg4,cfg4d,cfg5] [--out profiles/parity_r02.json]
+    python tools/parity_full.py --configs cfg1f32,cfg1rrf32,cfg2f32,cfg3f32,cfg4df32,cfg5f32 \
+        --out profiles/parity_f32_r02.json     # float32 twins (gates: see check())
 
 Per config it records (and `check()` gates, SURVEY.md §8c / north_star):
   * sigma: normwise max|ds_i|/s_1 per matrix <= 1e-12 (f64) -- the hard gate; per-value relative
@@ -43,6 +45,11 @@ CONFIGS = {
     "cfg4d": dict(kind="block", method="direct", tol=1e-13, m=256, n=256, batch=1000, seed=4_000_000),
     "cfg5": dict(kind="rsvd", m=128, n=128, batch=10_000, seed=5_000_000, k=32, p=8, rsvd_seed=5),
 }
+# float32 twins (north_star: "fp64/fp32 matrices"; sigma gate 1e-5 normwise): the same shapes, inputs
+# drawn from numpy's float32 stream (rsvd: the f64 test matrices rounded), default f32 tolerances
+for _k in ("cfg1", "cfg1rr", "cfg2", "cfg3", "cfg4d", "cfg5"):
+    CONFIGS[_k + "f32"] = dict(CONFIGS[_k], dtype="f32")
+CONFIGS["cfg4df32"]["tol"] = None  # blockjacobi.py:19-22 default, 1e-5 for float32
 
 
 def host_threads():
@@ -73,7 +80,7 @@ def dist(x):
     return {"p50": float(np.percentile(x, 50)), "p99": float(np.percentile(x, 99)), "max": float(np.max(x))}
 
 
-def vec_mismatch_batch(x, x_ref, s_ref, factor=256.0, ncols=None):
+def vec_mismatch_batch(x, x_ref, s_ref, factor=256.0, ncols=None, eps=EPS64):
     """x, x_ref: (B, rows, n) column vectors; s_ref (B, n) descending. Worst err/tol per matrix
     (<= 1 passes): columns compared up to sign, tol = factor eps s1/gap_j (Davis-Kahan)."""
     x = np.asarray(x, np.float64)
@@ -89,11 +96,11 @@ def vec_mismatch_batch(x, x_ref, s_ref, factor=256.0, ncols=None):
         gap[:, :-1] = np.minimum(gap[:, :-1], d)
     else:
         gap[:] = s1
-    ok = (s > s1 * 1e3 * EPS64) & (gap > s1 * 1e3 * EPS64)
+    ok = (s > s1 * 1e3 * eps) & (gap > s1 * 1e3 * eps)
     ok[:, nc:] = False
     sign = np.where(np.einsum("brn,brn->bn", x, x_ref) >= 0, 1.0, -1.0)
     err = np.max(np.abs(x * sign[:, None, :] - x_ref), axis=1)
-    tol = factor * EPS64 * s1 / np.where(np.isfinite(gap), gap, s1)
+    tol = factor * eps * s1 / np.where(np.isfinite(gap), gap, s1)
     ratio = np.where(ok, err / tol, 0.0)
     return np.max(ratio, axis=1) if n else np.zeros(B)
 
@@ -128,6 +135,29 @@ def recon_res(a, u, s, v):
     return np.sqrt(np.sum(d * d, axis=(1, 2))) / np.where(na > 0, na, 1.0)
 
 
+def exact_normwise(a, s, chunk=2000):
+    """Per-matrix max|s_i - s_exact_i| / s_exact_1, s_exact = LAPACK (numpy gesdd) in float64 on
+    the same input (for float32 twins: how far each implementation is from the exact values)."""
+    out = []
+    for i in range(0, a.shape[0], chunk):
+        sl = np.linalg.svd(np.asarray(a[i:i + chunk], np.float64), compute_uv=False)
+        ss = np.asarray(s[i:i + chunk, : sl.shape[1]], np.float64)
+        out.append(np.max(np.abs(ss - sl), axis=1) / np.maximum(sl[:, 0], 1e-300))
+    return np.concatenate(out) if out else np.zeros(0)
+
+
+def ref_fixture(name):
+    """The reference's own per-entry float32 results on the same inputs (tools/ref_runs/f32_ref.py,
+    run where /root/reference exists; committed as tests/golden/ref_f32_stats.npz)."""
+    path = os.path.join(ROOT, "tests", "golden", "ref_f32_stats.npz")
+    if not os.path.exists(path):
+        return None
+    z = np.load(path)
+    if f"{name}/index" not in z:
+        return None
+    return {k.split("/", 1)[1]: z[k] for k in z.files if k.startswith(name + "/")}
+
+
 def lapack_floor(a, s_ref, chunk=2000):
     """Per-value relative difference of the oracle's sigma from LAPACK's (numpy gesdd)."""
     out = []
@@ -145,10 +175,16 @@ def lapack_floor(a, s_ref, chunk=2000):
 def _inputs(name, c, dev):
     import paper_1707_05141_b200 as bf
 
+    import torch
+
+    f32 = c.get("dtype") == "f32"
     if c["kind"] == "rsvd":
         a, _ = bf.make_matrix_tensor(c["batch"], c["m"], c["n"], 1e16, rank=64, seed=c["seed"], device=dev)
+        if f32:
+            a = a.transpose(1, 2).float().contiguous().transpose(1, 2)
     else:
-        a = bf.gaussian_tensor(c["batch"], c["m"], c["n"], c["seed"], seed_mode="add", device=dev)
+        a = bf.gaussian_tensor(c["batch"], c["m"], c["n"], c["seed"], seed_mode="add",
+                               dtype=torch.float32 if f32 else torch.float64, device=dev)
     return a  # (B, m, n) view of column-major storage
 
 
@@ -167,7 +203,9 @@ def run_config(name, threads, dev="cuda"):
     a = _inputs(name, c, dev)
     a_np = _np(a)  # (B, m, n)
     a3 = np.ascontiguousarray(a_np.transpose(0, 2, 1))  # per-matrix column-major for the oracle
-    rec = {"config": name, "batch": B, "m": m, "n": n}
+    f32 = c.get("dtype") == "f32"
+    eps = float(np.finfo(np.float32 if f32 else np.float64).eps)
+    rec = {"config": name, "batch": B, "m": m, "n": n, "dtype": "f32" if f32 else "f64"}
     t0 = time.perf_counter()
     if c["kind"] == "qr":
         q, r = bf.qr_tensor(a)
@@ -178,8 +216,8 @@ def run_config(name, threads, dev="cuda"):
         q_g, r_g = _np(q), _np(r)
         q_o, r_o = qo.transpose(0, 2, 1), ro.transpose(0, 2, 1)
         scale = np.sqrt(np.sum(a_np * a_np, axis=(1, 2)))
-        dq = np.max(np.abs(q_g - q_o), axis=(1, 2)) / (EPS64 * np.maximum(scale, 1.0))
-        dr = np.max(np.abs(r_g - r_o), axis=(1, 2)) / (EPS64 * np.maximum(scale, 1.0))
+        dq = np.max(np.abs(q_g - q_o), axis=(1, 2)) / (eps * np.maximum(scale, 1.0))
+        dr = np.max(np.abs(r_g - r_o), axis=(1, 2)) / (eps * np.maximum(scale, 1.0))
         qr_g = np.matmul(q_g, r_g)
         qr_o = np.matmul(q_o, r_o)
         rec.update({
@@ -212,13 +250,14 @@ def run_config(name, threads, dev="cuda"):
         floor = lapack_floor(a_np, s_o)
         gpu_floor = lapack_floor(a_np, s_g)
         fac = 256.0 if c["kind"] == "svd" else 4096.0
-        um = vec_mismatch_batch(u_g, u_o, s_o, fac)
-        vm = vec_mismatch_batch(v_g, v_o, s_o, fac)
+        um = vec_mismatch_batch(u_g, u_o, s_o, fac, eps=eps)
+        vm = vec_mismatch_batch(v_g, v_o, s_o, fac, eps=eps)
         dsw = sw_g - sw_o
         odd = np.flatnonzero((cv_g != cv_o) | (np.abs(dsw) > 1))
         chaotic = []
+        tol = c.get("tol") or (1e-5 if f32 else 1e-13)
         if c["kind"] == "block":
-            eh_all_g, tol = _np(r["e_history"]), c["tol"]
+            eh_all_g = _np(r["e_history"])
             for b in odd:
                 eo = o["e_history"][b, : sw_o[b]]
                 eg = eh_all_g[b, : sw_g[b]]
@@ -242,6 +281,26 @@ def run_config(name, threads, dev="cuda"):
             "recon": res_pair(recon_res(a_np, u_g, s_g, v_g), recon_res(a_np, u_o, s_o, v_o), chaotic),
             "chaotic_entries": chaotic,
         })
+        if f32:
+            # float32: the oracle's own distance from the exact singular values can exceed the
+            # 1e-5 gate (block direct, tol 1e-5); record both distances per matrix
+            ge, oe = exact_normwise(a_np, s_g), exact_normwise(a_np, s_o)
+            rec["sigma_normwise_vs_exact"] = {"gpu": dist(ge), "oracle": dist(oe)}
+            rec["sigma_f32_fail"] = int(np.sum((normwise > 1e-5) & (ge > oe)))
+            fx = ref_fixture(name)
+            if fx is not None:
+                idx = fx["index"]
+                d = sw_g[idx] - fx["sweeps"]
+                rec["vs_reference"] = {
+                    "entries": int(idx.size),
+                    "sweeps_gpu_minus_ref_hist": {str(k): int(v) for k, v in zip(*np.unique(d, return_counts=True))},
+                    "sweeps_oracle_minus_ref_hist": {
+                        str(k): int(v) for k, v in zip(*np.unique(sw_o[idx] - fx["sweeps"], return_counts=True))},
+                    "converged_equal": int(np.sum(cv_g[idx] == fx["converged"])),
+                    "ref_max": {"orth_u": float(fx["orth_u"].max()), "orth_v": float(fx["orth_v"].max()),
+                                "recon": float(fx["recon"].max())},
+                    "full_batch": bool(idx.size == B),
+                }
         # entries whose flags or sweep counts differ beyond +-1, with the e history that explains them
         rec["flag_or_sweep_outliers"] = []
         for b in odd[:300]:
@@ -250,7 +309,6 @@ def run_config(name, threads, dev="cuda"):
             if c["kind"] == "block":
                 eo = o["e_history"][b, : sw_o[b]]
                 eg = _np(r["e_history"])[b, : sw_g[b]]
-                tol = c["tol"]
                 item["oracle_e_over_tol_last5"] = [float(x / tol) for x in eo[-5:]]
                 item["gpu_e_over_tol_last5"] = [float(x / tol) for x in eg[-5:]]
                 item["marginal"] = int(b) in chaotic
@@ -276,8 +334,8 @@ def run_config(name, threads, dev="cuda"):
         u_o, s_o, v_o = o["u"].transpose(0, 2, 1), o["s"], o["v"].transpose(0, 2, 1)
         normwise, per_value = sigma_stats(s_g, s_o)
         k = c["k"]
-        um = vec_mismatch_batch(u_g, u_o, s_o, 4096.0, ncols=k)
-        vm = vec_mismatch_batch(v_g, v_o, s_o, 4096.0, ncols=k)
+        um = vec_mismatch_batch(u_g, u_o, s_o, 4096.0, ncols=k, eps=eps)
+        vm = vec_mismatch_batch(v_g, v_o, s_o, 4096.0, ncols=k, eps=eps)
         _, pv_k = sigma_stats(s_g[:, :k], s_o[:, :k])
         rec.update({
             "sigma_normwise": dist(normwise), "sigma_per_value_rel": dist(per_value),
@@ -305,6 +363,15 @@ def check(rec):
 
     def res_gate(key):
         g, o = rec[key]["gpu_max"], rec[key]["oracle_max"]
+        if rec.get("dtype") == "f32":
+            # float32 residuals sit at the stopping tolerance (pairs left just under tol); the maxima
+            # of the reference and of its C restatement themselves differ by ~1 % (cfg1f32: 9.15e-6
+            # vs 9.08e-6, cfg3f32: 1.757e-5 vs 1.736e-5, profiles/f32_ref_r02.json), so "no worse"
+            # is judged against the larger of the two with a 2 % band
+            vr = rec.get("vs_reference")
+            if vr and vr["full_batch"]:
+                o = max(o, vr["ref_max"].get(key, o))
+            o *= 1.02
         if g > o:
             bad.append(f"{name}: {key} gpu max {g:.3e} > oracle max {o:.3e}")
 
@@ -316,7 +383,15 @@ def check(rec):
         res_gate("orth_q")
         res_gate("recon")
         return bad
-    if rec["sigma_normwise"]["max"] > 1e-12:
+    f32 = rec.get("dtype") == "f32"
+    if f32:
+        # float32 (north_star: 1e-5): within 1e-5 normwise of the oracle, or closer to the exact
+        # singular values than the oracle is (the reference's own float32 error can exceed 1e-5)
+        nfail = rec.get("sigma_f32_fail", int(rec["sigma_normwise"]["max"] > 1e-5))
+        if nfail:
+            bad.append(f"{name}: {nfail} matrices with sigma > 1e-5 from the oracle and farther "
+                       "from exact than the oracle")
+    elif rec["sigma_normwise"]["max"] > 1e-12:
         bad.append(f"{name}: sigma normwise {rec['sigma_normwise']['max']:.3e} > 1e-12")
     if kind == "rsvd":
         if rec["u_mismatch_ratio_top_k"]["max"] > 1 or rec["v_mismatch_ratio_top_k"]["max"] > 1:
@@ -331,6 +406,11 @@ def check(rec):
         # (profiles/cfg4_chaos_r02.json), so these are "chaotic": reported, capped at 10 % of the
         # batch, and left out of the gated residual maxima (their residuals are listed as *_all).
         outl = rec["flag_or_sweep_outliers"]
+        if f32:
+            # float32 at the default tolerance (1e-6 / 1e-5) converges at the rounding noise floor:
+            # the reference and its restatement differ by 2 sweeps on 9 of 5000 cfg3f32 entries
+            # (profiles/f32_ref_r02.json); float32 twins gate flags equal and sweeps within +-2
+            outl = [o for o in outl if o["conv_gpu"] != o["conv_oracle"] or abs(o["sweeps_gpu"] - o["sweeps_oracle"]) > 2]
         hard = [o for o in outl if not o.get("marginal", False)]
         if hard:
             bad.append(f"{name}: {len(hard)} entries with converged flags / sweeps (+-1) differing, first {hard[0]}")
@@ -343,7 +423,7 @@ def check(rec):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--configs", default=",".join(CONFIGS))
+    ap.add_argument("--configs", default=",".join(k for k in CONFIGS if not k.endswith("f32")))
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "parity_r02.json"))
     ap.add_argument("--threads", type=int, default=host_threads())
     args = ap.parse_args()
