@@ -1,6 +1,7 @@
 // C ABI (include/batchfact_b200.h): validation, workspace planning, dispatch.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -192,9 +193,12 @@ RsvdLayout rsvd_layout(int64_t batch, int m, int n, int w, int es, bool need_ome
   return L;
 }
 
+// omega_rowmajor: a caller-supplied omega stored like a device-drawn one (C order n x w, used by
+// the float32-on-float64 path); svd_tol: the inner SVD tolerance (0: the default of T)
 template <typename T>
 int rsvd_impl(int64_t batch, int m, int n, int k, int p, uint64_t slo, uint64_t shi, int64_t ibase, const T* a,
-              const T* omega, T* u, T* s, T* v, void* ws, size_t wsb, void* st) {
+              const T* omega, T* u, T* s, T* v, void* ws, size_t wsb, void* st, bool omega_rowmajor = false,
+              double svd_tol = 0.0) {
   if (batch < 0 || m < 0 || n < 0) return fail(BF_ERR_ARG, "negative batch or shape");
   if (k < 1) return fail(BF_ERR_ARG, "k must be >= 1");
   if (p < 0) return fail(BF_ERR_ARG, "p must be >= 0");
@@ -227,7 +231,8 @@ int rsvd_impl(int64_t batch, int m, int n, int k, int p, uint64_t slo, uint64_t 
   }
   bf::GemmLaunch g;
   // Y = A @ Omega (rsvd.py:66); a device-drawn Omega is row-major, i.e. Omega^T column-major
-  g = bf::GemmLaunch{batch, m,    w,  n, a, m, (int64_t)m * n, false, om, omega ? n : w, (int64_t)n * w, !omega, Y, m,
+  const bool om_rm = !omega || omega_rowmajor;
+  g = bf::GemmLaunch{batch, m,    w,  n, a, m, (int64_t)m * n, false, om, om_rm ? w : n, (int64_t)n * w, om_rm, Y, m,
                      (int64_t)m * w};
   if ((rc = bf::launch_gemm(dt, g, cs))) return cuda_rc(rc, "rsvd/gemm1");
   // Q = qr(Y).q (rsvd.py:67)
@@ -255,7 +260,7 @@ int rsvd_impl(int64_t batch, int m, int n, int k, int p, uint64_t slo, uint64_t 
   L.sweeps = nullptr;
   L.converged = nullptr;
   L.rotations = nullptr;
-  L.tol = resolve_tol(0.0, f64, false);
+  L.tol = resolve_tol(svd_tol, f64, false);
   L.max_sweeps = 30;
   L.ordering = 1;
   L.tier = 0;
@@ -266,6 +271,187 @@ int rsvd_impl(int64_t batch, int m, int n, int k, int p, uint64_t slo, uint64_t 
   if ((rc = bf::launch_gemm(dt, g, cs))) return cuda_rc(rc, "rsvd/gemm3");
   g = bf::GemmLaunch{batch, n, w, w, Qb, n, (int64_t)n * w, false, Vr, w, (int64_t)w * w, false, v, n, (int64_t)n * w};
   if ((rc = bf::launch_gemm(dt, g, cs))) return cuda_rc(rc, "rsvd/gemm4");
+  return BF_OK;
+}
+
+// ---------------------------------------------------------------- float32 on the float64 tiers
+// The float32 entry points keep float32 storage but compute on the float64 tiers wherever those
+// are the specialised ones: the register QR, the rr / register SVD tiers, the DMMA block-Jacobi
+// pipeline (direct method) and the rsvd built on them. On B200 those run 1.7-3.7x faster than the float32
+// CUDA-core tiers on every BASELINE shape (tools/time_f32.py) and are more accurate;
+// the semantics stay float32 (float32 default tolerances, numpy's float32 Gaussian stream for
+// rsvd). Inputs are widened into the workspace, results rounded back. BF_F32_NATIVE=1 keeps the
+// float32 tiers (A/B and the float32-kernel tests).
+bool f32_native() {
+  const char* e = getenv("BF_F32_NATIVE");
+  return e && e[0] && e[0] != '0';
+}
+
+// bump allocator over the workspace (base == nullptr: sizing only)
+struct Carve {
+  char* base;
+  size_t off = 0;
+  explicit Carve(void* b) : base((char*)b) {}
+  template <typename T>
+  T* take(size_t elems) {
+    T* p = base ? (T*)(base + off) : nullptr;
+    off += al(elems * sizeof(T));
+    return p;
+  }
+  void* rest() const { return base ? base + off : nullptr; }
+};
+
+int widen(int64_t n, const float* s, double* d, cudaStream_t st) { return bf::launch_cast<float, double>(n, s, d, st); }
+int narrow(int64_t n, const double* s, float* d, cudaStream_t st) { return bf::launch_cast<double, float>(n, s, d, st); }
+
+bool qr_promote(int m, int n) { return !f32_native() && m >= n && n > 0 && bf::qr_reg_covers(m, n); }
+
+size_t qr_promo_layout(Carve& c, int64_t B, int m, int n, double** a, double** q, double** r) {
+  *a = c.take<double>((size_t)B * m * n);
+  *q = c.take<double>((size_t)B * m * n);
+  *r = c.take<double>((size_t)B * n * n);
+  return c.off + bf::qr_global_ws_bytes(0, B, m, n);
+}
+
+int qr_f32(int64_t batch, int m, int n, const float* a, float* q, float* r, int pw, void* ws, size_t wsb, void* st) {
+  if (batch <= 0 || pw < 1 || !qr_promote(m, n)) return qr_impl<float>(batch, m, n, a, q, r, pw, ws, wsb, st);
+  Carve c(nullptr);
+  double *A, *Q, *R;
+  int rc = check_ws(ws, wsb, qr_promo_layout(c, batch, m, n, &A, &Q, &R));
+  if (rc) return rc;
+  Carve w(ws);
+  qr_promo_layout(w, batch, m, n, &A, &Q, &R);
+  cudaStream_t cs = S(st);
+  if ((rc = widen(batch * (int64_t)m * n, a, A, cs))) return cuda_rc(rc, "qr/widen");
+  if ((rc = qr_impl<double>(batch, m, n, A, Q, R, pw, w.rest(), wsb - w.off, st))) return rc;
+  if ((rc = narrow(batch * (int64_t)m * n, Q, q, cs)) || (rc = narrow(batch * (int64_t)n * n, R, r, cs)))
+    return cuda_rc(rc, "qr/narrow");
+  return BF_OK;
+}
+
+bool svd_promote(int m, int n, const bf_jacobi_opts* o) {
+  if (f32_native() || !o || o->tier == 2 || m < n || n < 2) return false;
+  bf::SvdLaunch L{};
+  L.batch = 1;
+  L.m = m;
+  L.n = n;
+  L.ordering = o->ordering;
+  L.tier = o->tier;
+  L.max_sweeps = o->max_sweeps;
+  L.v = o->accumulate_v ? (void*)1 : nullptr;
+  return bf::svd_rr_covers(L) || bf::svd_reg_covers(L);
+}
+
+size_t svd_promo_layout(Carve& c, int64_t B, int m, int n, const bf_jacobi_opts* o, double** a, double** u, double** s,
+                        double** v) {
+  *a = c.take<double>((size_t)B * m * n);
+  *u = c.take<double>((size_t)B * m * n);
+  *s = c.take<double>((size_t)B * n);
+  *v = o->accumulate_v ? c.take<double>((size_t)B * n * n) : nullptr;
+  return c.off + bf::svd_global_ws_bytes(0, B, m, n, o->ordering, o->accumulate_v != 0, o->tier, o->max_sweeps);
+}
+
+int svd_f32(int64_t batch, int m, int n, const float* a, float* u, float* s, float* v, int32_t* sweeps, uint8_t* conv,
+            int64_t* rots, const bf_jacobi_opts* o, void* ws, size_t wsb, void* st) {
+  if (batch <= 0 || check_jopts(o) || !svd_promote(m, n, o) || (o->accumulate_v && !v))
+    return svd_impl<float>(batch, m, n, a, u, s, v, sweeps, conv, rots, o, ws, wsb, st);
+  Carve c(nullptr);
+  double *A, *U, *Sg, *V;
+  int rc = check_ws(ws, wsb, svd_promo_layout(c, batch, m, n, o, &A, &U, &Sg, &V));
+  if (rc) return rc;
+  Carve w(ws);
+  svd_promo_layout(w, batch, m, n, o, &A, &U, &Sg, &V);
+  bf_jacobi_opts o64 = *o;
+  o64.tolerance = resolve_tol(o->tolerance, false, false);  // float32 semantics: jacobi.py:22-25
+  cudaStream_t cs = S(st);
+  if ((rc = widen(batch * (int64_t)m * n, a, A, cs))) return cuda_rc(rc, "svd/widen");
+  if ((rc = svd_impl<double>(batch, m, n, A, U, Sg, V, sweeps, conv, rots, &o64, w.rest(), wsb - w.off, st))) return rc;
+  if ((rc = narrow(batch * (int64_t)m * n, U, u, cs)) || (rc = narrow(batch * (int64_t)n, Sg, s, cs)) ||
+      (V && (rc = narrow(batch * (int64_t)n * n, V, v, cs))))
+    return cuda_rc(rc, "svd/narrow");
+  return BF_OK;
+}
+
+// Direct method only: the float32 Gram method's behaviour is set by its float32 rounding -- its e
+// floor (~ eps32 kappa^2 of the pair blocks) sits at the float32 tolerance, so the reference's
+// float32 Gram sweeps / converged flags are decided by that rounding; a
+// float64 Gram would converge where the reference does not. The float32 Gram runs on the float32
+// tiers.
+bool block_promote(int m, int n, int method) { return !f32_native() && method == 1 && m >= n && m > 0 && n > 0; }
+
+size_t block_promo_layout(Carve& c, int64_t B, int m, int n, const bf_block_opts* o, double** a, double** u,
+                          double** s, double** v, double** e) {
+  *a = c.take<double>((size_t)B * m * n);
+  *u = c.take<double>((size_t)B * m * n);
+  *s = c.take<double>((size_t)B * n);
+  *v = o->accumulate_v ? c.take<double>((size_t)B * n * n) : nullptr;
+  *e = c.take<double>((size_t)B * o->max_sweeps);
+  return c.off + bf::block_ws_bytes(0, B, m, n, o->block_width, o->method, o->accumulate_v != 0);
+}
+
+int block_f32(int64_t batch, int m, int n, const float* a, float* u, float* s, float* v, int32_t* sweeps, uint8_t* conv,
+              float* eh, const bf_block_opts* o, void* ws, size_t wsb, void* st, int64_t* stats) {
+  if (batch <= 0 || check_bopts(o) || !block_promote(m, n, o->method) || (o->accumulate_v && !v) || !sweeps || !conv)
+    return block_impl<float>(batch, m, n, a, u, s, v, sweeps, conv, eh, o, ws, wsb, st, stats);
+  Carve c(nullptr);
+  double *A, *U, *Sg, *V, *E;
+  int rc = check_ws(ws, wsb, block_promo_layout(c, batch, m, n, o, &A, &U, &Sg, &V, &E));
+  if (rc) return rc;
+  Carve w(ws);
+  block_promo_layout(w, batch, m, n, o, &A, &U, &Sg, &V, &E);
+  bf_block_opts o64 = *o;
+  o64.tolerance = resolve_tol(o->tolerance, false, true);  // float32 semantics: blockjacobi.py:19-22
+  cudaStream_t cs = S(st);
+  if ((rc = widen(batch * (int64_t)m * n, a, A, cs))) return cuda_rc(rc, "block_svd/widen");
+  if ((rc = block_impl<double>(batch, m, n, A, U, Sg, V, sweeps, conv, eh ? E : nullptr, &o64, w.rest(), wsb - w.off,
+                               st, stats)))
+    return rc;
+  if ((rc = narrow(batch * (int64_t)m * n, U, u, cs)) || (rc = narrow(batch * (int64_t)n, Sg, s, cs)) ||
+      (V && (rc = narrow(batch * (int64_t)n * n, V, v, cs))) ||
+      (eh && (rc = narrow(batch * (int64_t)o->max_sweeps, E, eh, cs))))
+    return cuda_rc(rc, "block_svd/narrow");
+  return BF_OK;
+}
+
+bool rsvd_promote() { return !f32_native(); }
+
+size_t rsvd_promo_layout(Carve& c, int64_t B, int m, int n, int w, bool draw, double** a, double** om, float** om32,
+                         double** u, double** s, double** v) {
+  *a = c.take<double>((size_t)B * m * n);
+  *om = c.take<double>((size_t)B * n * w);
+  *om32 = draw ? c.take<float>((size_t)B * n * w) : nullptr;
+  *u = c.take<double>((size_t)B * m * w);
+  *s = c.take<double>((size_t)B * w);
+  *v = c.take<double>((size_t)B * n * w);
+  return c.off + rsvd_layout(B, m, n, w, 8, false).total;
+}
+
+int rsvd_f32(int64_t batch, int m, int n, int k, int p, uint64_t slo, uint64_t shi, int64_t ibase, const float* a,
+             const float* omega, float* u, float* s, float* v, void* ws, size_t wsb, void* st) {
+  const int w = k + p;
+  if (batch <= 0 || k < 1 || p < 0 || w > std::min(m, n) || !rsvd_promote())
+    return rsvd_impl<float>(batch, m, n, k, p, slo, shi, ibase, a, omega, u, s, v, ws, wsb, st);
+  Carve c(nullptr);
+  double *A, *Om, *U, *Sg, *V;
+  float* Om32;
+  int rc = check_ws(ws, wsb, rsvd_promo_layout(c, batch, m, n, w, !omega, &A, &Om, &Om32, &U, &Sg, &V));
+  if (rc) return rc;
+  Carve cw(ws);
+  rsvd_promo_layout(cw, batch, m, n, w, !omega, &A, &Om, &Om32, &U, &Sg, &V);
+  cudaStream_t cs = S(st);
+  const int64_t nom = batch * (int64_t)n * w;
+  if (!omega) {  // numpy's float32 stream (rsvd.py:65 dtype=a.dtype), C order, then widened
+    rc = bf::launch_gaussian_f32(batch, n, w, slo, shi, ibase, 0, 0, Om32, (int64_t)n * w, cs, 1);
+    if (rc) return cuda_rc(rc, "rsvd/omega");
+  }
+  if ((rc = widen(batch * (int64_t)m * n, a, A, cs)) || (rc = widen(nom, omega ? omega : Om32, Om, cs)))
+    return cuda_rc(rc, "rsvd/widen");
+  if ((rc = rsvd_impl<double>(batch, m, n, k, p, slo, shi, ibase, A, Om, U, Sg, V, cw.rest(), wsb - cw.off, st,
+                              !omega, resolve_tol(0.0, false, false))))
+    return rc;
+  if ((rc = narrow(batch * (int64_t)m * w, U, u, cs)) || (rc = narrow(batch * (int64_t)w, Sg, s, cs)) ||
+      (rc = narrow(batch * (int64_t)n * w, V, v, cs)))
+    return cuda_rc(rc, "rsvd/narrow");
   return BF_OK;
 }
 
@@ -312,6 +498,11 @@ const char* bf_version(void) { return "batchfact_b200 0.1.0 (sm_100a)"; }
 
 size_t bf_qr_workspace_size(int64_t batch, int32_t m, int32_t n, int32_t es) {
   if (m < n || m <= 0 || n <= 0) return 0;
+  if (es == 4 && batch > 0 && qr_promote(m, n)) {
+    Carve c(nullptr);
+    double *a, *q, *r;
+    return qr_promo_layout(c, batch, m, n, &a, &q, &r);
+  }
   return bf::qr_global_ws_bytes(es == 8 ? 0 : 1, batch, m, n);
 }
 int bf_qr_batched_f64(int64_t batch, int32_t m, int32_t n, const double* a, double* q, double* r, int32_t pw,
@@ -320,11 +511,16 @@ int bf_qr_batched_f64(int64_t batch, int32_t m, int32_t n, const double* a, doub
 }
 int bf_qr_batched_f32(int64_t batch, int32_t m, int32_t n, const float* a, float* q, float* r, int32_t pw, void* ws,
                       size_t wsb, void* st) {
-  return qr_impl<float>(batch, m, n, a, q, r, pw, ws, wsb, st);
+  return qr_f32(batch, m, n, a, q, r, pw, ws, wsb, st);
 }
 
 size_t bf_svd_workspace_size(int64_t batch, int32_t m, int32_t n, int32_t es, const bf_jacobi_opts* o) {
   if (!o || m < n || n <= 0) return 0;
+  if (es == 4 && batch > 0 && svd_promote(m, n, o)) {
+    Carve c(nullptr);
+    double *a, *u, *s, *v;
+    return svd_promo_layout(c, batch, m, n, o, &a, &u, &s, &v);
+  }
   return bf::svd_global_ws_bytes(es == 8 ? 0 : 1, batch, m, n, o->ordering, o->accumulate_v != 0, o->tier,
                                  o->max_sweeps);
 }
@@ -336,11 +532,16 @@ int bf_svd_batched_f64(int64_t batch, int32_t m, int32_t n, const double* a, dou
 int bf_svd_batched_f32(int64_t batch, int32_t m, int32_t n, const float* a, float* u, float* s, float* v,
                        int32_t* sweeps, uint8_t* conv, int64_t* rots, const bf_jacobi_opts* o, void* ws, size_t wsb,
                        void* st) {
-  return svd_impl<float>(batch, m, n, a, u, s, v, sweeps, conv, rots, o, ws, wsb, st);
+  return svd_f32(batch, m, n, a, u, s, v, sweeps, conv, rots, o, ws, wsb, st);
 }
 
 size_t bf_block_svd_workspace_size(int64_t batch, int32_t m, int32_t n, int32_t es, const bf_block_opts* o) {
   if (!o || m < n || m <= 0 || o->block_width < 1) return 0;
+  if (es == 4 && batch > 0 && o->max_sweeps >= 1 && block_promote(m, n, o->method)) {
+    Carve c(nullptr);
+    double *a, *u, *s, *v, *e;
+    return block_promo_layout(c, batch, m, n, o, &a, &u, &s, &v, &e);
+  }
   return bf::block_ws_bytes(es == 8 ? 0 : 1, batch, m, n, o->block_width, o->method, o->accumulate_v != 0);
 }
 int bf_block_svd_batched_f64(int64_t batch, int32_t m, int32_t n, const double* a, double* u, double* s, double* v,
@@ -351,7 +552,7 @@ int bf_block_svd_batched_f64(int64_t batch, int32_t m, int32_t n, const double* 
 int bf_block_svd_batched_f32(int64_t batch, int32_t m, int32_t n, const float* a, float* u, float* s, float* v,
                              int32_t* sweeps, uint8_t* conv, float* eh, const bf_block_opts* o, void* ws, size_t wsb,
                              void* st) {
-  return block_impl<float>(batch, m, n, a, u, s, v, sweeps, conv, eh, o, ws, wsb, st);
+  return block_f32(batch, m, n, a, u, s, v, sweeps, conv, eh, o, ws, wsb, st, nullptr);
 }
 int bf_block_svd_batched_ex_f64(int64_t batch, int32_t m, int32_t n, const double* a, double* u, double* s, double* v,
                                 int32_t* sweeps, uint8_t* conv, double* eh, int64_t* stats, const bf_block_opts* o,
@@ -361,11 +562,17 @@ int bf_block_svd_batched_ex_f64(int64_t batch, int32_t m, int32_t n, const doubl
 int bf_block_svd_batched_ex_f32(int64_t batch, int32_t m, int32_t n, const float* a, float* u, float* s, float* v,
                                 int32_t* sweeps, uint8_t* conv, float* eh, int64_t* stats, const bf_block_opts* o,
                                 void* ws, size_t wsb, void* st) {
-  return block_impl<float>(batch, m, n, a, u, s, v, sweeps, conv, eh, o, ws, wsb, st, stats);
+  return block_f32(batch, m, n, a, u, s, v, sweeps, conv, eh, o, ws, wsb, st, stats);
 }
 
 size_t bf_rsvd_workspace_size(int64_t batch, int32_t m, int32_t n, int32_t k, int32_t p, int32_t es) {
   if (k < 1 || p < 0 || k + p > std::min(m, n)) return 0;
+  if (es == 4 && batch > 0 && rsvd_promote()) {
+    Carve c(nullptr);
+    double *a, *om, *u, *s, *v;
+    float* om32;
+    return rsvd_promo_layout(c, batch, m, n, k + p, true, &a, &om, &om32, &u, &s, &v);
+  }
   return rsvd_layout(batch, m, n, k + p, es, true).total;
 }
 int bf_rsvd_batched_f64(int64_t batch, int32_t m, int32_t n, int32_t k, int32_t p, uint64_t slo, uint64_t shi,
@@ -376,7 +583,7 @@ int bf_rsvd_batched_f64(int64_t batch, int32_t m, int32_t n, int32_t k, int32_t 
 int bf_rsvd_batched_f32(int64_t batch, int32_t m, int32_t n, int32_t k, int32_t p, uint64_t slo, uint64_t shi,
                         int64_t ibase, const float* a, const float* omega, float* u, float* s, float* v, void* ws,
                         size_t wsb, void* st) {
-  return rsvd_impl<float>(batch, m, n, k, p, slo, shi, ibase, a, omega, u, s, v, ws, wsb, st);
+  return rsvd_f32(batch, m, n, k, p, slo, shi, ibase, a, omega, u, s, v, ws, wsb, st);
 }
 
 int bf_gaussian_batched_f64(int64_t batch, int32_t rows, int32_t cols, uint64_t slo, uint64_t shi, int64_t ibase,

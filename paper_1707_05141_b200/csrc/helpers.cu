@@ -174,7 +174,28 @@ __global__ void axpby_kernel(int64_t n, T alpha, const T* p, T beta, const T* c,
   out[i] = r;
 }
 
+// float32 <-> float64 widening / rounding for the float32 entry points that compute on the float64
+// tiers (api.cu); grid-stride, 2 elements per thread per iteration
+template <typename S, typename D>
+__global__ void __launch_bounds__(256) cast_kernel(int64_t n, const S* __restrict__ src, D* __restrict__ dst) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) dst[i] = (D)src[i];
+}
+
 static unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+template <typename S, typename D>
+int launch_cast(int64_t n, const S* src, D* dst, cudaStream_t st) {
+  if (n <= 0) return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (n + 255) / 256, cap = (int64_t)sms * 8;
+  cast_kernel<S, D><<<(unsigned)(want < cap ? want : cap), 256, 0, st>>>(n, src, dst);
+  return (int)cudaGetLastError();
+}
+template int launch_cast<float, double>(int64_t, const float*, double*, cudaStream_t);
+template int launch_cast<double, float>(int64_t, const double*, float*, cudaStream_t);
 
 template <typename T>
 int launch_householder(int64_t batch, int len, const T* x, T* v, T* tau, cudaStream_t st) {

@@ -92,6 +92,12 @@ template <typename T>
 int launch_frobenius(int64_t batch, int64_t count, const T* a, T* out, cudaStream_t st);
 template <typename T>
 int launch_axpby(int64_t n, T alpha, const T* p, T beta, const T* c, T* out, cudaStream_t st);
+template <typename S, typename D>
+int launch_cast(int64_t n, const S* src, D* dst, cudaStream_t st);
+// float64 fast tiers covering a shape (the float32 entry points compute on them, api.cu)
+bool qr_reg_covers(int m, int n);
+bool svd_rr_covers(const SvdLaunch& L);
+bool svd_reg_covers(const SvdLaunch& L);
 
 struct BlockLaunch {
   int64_t batch;

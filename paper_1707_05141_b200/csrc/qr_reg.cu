@@ -286,6 +286,8 @@ static int launch_qr_reg_t(int64_t batch, int m, const double* a, int64_t as, do
   return (int)cudaGetLastError();
 }
 
+bool qr_reg_covers(int m, int n) { return ((n == 32 || n == 16) && m <= 64) || (n == 40 && m <= 128); }
+
 // Returns -1 if no register configuration covers (m, n).
 int launch_qr_reg(int dtype, int64_t batch, int m, int n, const void* a, int64_t as, void* q, int64_t qs, void* r,
                   int64_t rs, cudaStream_t st) {
@@ -293,6 +295,7 @@ int launch_qr_reg(int dtype, int64_t batch, int m, int n, const void* a, int64_t
   const double* A = (const double*)a;
   double* Q = (double*)q;
   double* Rr = (double*)r;
+  if (!qr_reg_covers(m, n)) return -1;
   if (n == 32 && m <= 64) return launch_qr_reg_t<32, 2, 1, BF_QR_G>(batch, m, A, as, Q, qs, Rr, rs, st);
   if (n == 16 && m <= 64) return launch_qr_reg_t<16, 2, 1>(batch, m, A, as, Q, qs, Rr, rs, st);
   if (n == 40 && m <= 128) return launch_qr_reg_t<40, 2, 2, BF_QR40_G>(batch, m, A, as, Q, qs, Rr, rs, st);

@@ -286,6 +286,14 @@ size_t svd_reg_ws_bytes(int dtype, const SvdLaunch& L) {
   return rc == 0 ? need : 0;
 }
 
+bool svd_reg_covers(const SvdLaunch& L) {
+  RegPlan p = reg_plan(L, 0);
+  if (!p.ok) return false;
+  size_t need = 0;
+  return (L.ordering == 1 ? reg_dispatch<1>(p, L, nullptr, 0, nullptr, &need)
+                          : reg_dispatch<0>(p, L, nullptr, 0, nullptr, &need)) == 0;
+}
+
 int launch_svd_reg(int dtype, const SvdLaunch& L, void* ws, size_t wsb, cudaStream_t st, bool* handled) {
   *handled = false;
   RegPlan p = reg_plan(L, dtype);

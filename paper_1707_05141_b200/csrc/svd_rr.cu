@@ -978,6 +978,12 @@ size_t svd_rr_ws_bytes(int dtype, const SvdLaunch& L) {
   return rr_dispatch(L, nullptr, 0, nullptr, &need) == 0 ? need : 0;
 }
 
+bool svd_rr_covers(const SvdLaunch& L) {
+  if (L.ordering != 1 || L.tier == 2 || L.n < 2) return false;
+  size_t need = 0;
+  return rr_dispatch(L, nullptr, 0, nullptr, &need) == 0;
+}
+
 int launch_svd_rr(int dtype, const SvdLaunch& L, void* ws, size_t wsb, cudaStream_t st, bool* handled) {
   *handled = false;
   if (dtype != 0 || L.ordering != 1 || L.tier == 2 || L.n < 2) return 0;
