@@ -8,6 +8,8 @@
 // Tiles: 256 threads, thread (ti, tj) owns entries (ti + 16a, tj + 16b), a, b < TT (kk = 16*TT),
 // so every shared-memory read in the inner loop is a broadcast or a 128-byte contiguous row.
 #pragma once
+#include <cuda.h>  // CUtensorMap (the tensor-map TMA variant; encoded on the host, block_kernels.cu)
+
 #include "common.cuh"
 
 namespace bf {
@@ -236,7 +238,23 @@ BF_DEV void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) 
 }
 BF_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-constexpr int kBlockTmaDefault = 0;  // measured: 1-D bulk staging is 1.4-3.5 % slower
+// 2-D tensor-map TMA (cp.async.bulk.tensor): W viewed as a (rows = m) x (cols = B * n_pad)
+// column-major tensor, box = 8 rows x 32 columns (one block's columns, 64 B of each), 64-byte
+// swizzle. One elected thread issues 2 blocks x (chunk rows / 8) boxes per chunk; rows past m
+// arrive as zeros (TMA out-of-bounds fill). In a [32 col][8 row] box the 16-byte chunk
+// r / 2 of column c sits at chunk (r / 2) ^ ((c / 2) & 3) (64B pattern, 512 B period), which
+// makes both fragment patterns below two wavefronts per warp load.
+BF_DEV void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+      ::"r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y) : "memory");
+}
+constexpr int kTmaBoxRows = 8, kTmaBoxCols = 32, kTmaBox = kTmaBoxRows * kTmaBoxCols;  // doubles per box
+BF_DEV int swz64(int c, int r) { return c * kTmaBoxRows + ((((r >> 1) ^ ((c >> 1) & 3)) << 1) | (r & 1)); }
+
+// BF_BLOCK_TMA bits: 1 / 2 = 1-D bulk staging of bj_gram_mma / bj_rot_mma, 4 / 8 = tensor-map
+// TMA Gram / rotation kernels (bj_gram_tma / bj_rot_tma)
+constexpr int kBlockTmaDefault = 12;  // tensor-map TMA kernels (measured: on par or 0.2-0.5 % faster than cp.async; 1-D bulk 1.4-3.5 % slower)
 constexpr int kMmaKK = 64;   // pair width 2k
 constexpr int kGramCH = 32;  // rows per staged chunk (8 k-steps)
 constexpr int kGramLD = kGramCH + 4;
@@ -290,15 +308,17 @@ __global__ void __launch_bounds__(256) bj_gram_mma(BJGemmArgs<double> a, int ste
         for (int e = tid; e < KK * (CH - rows); e += 256) stage[buf][(e / (CH - rows)) * LDR + rows + e % (CH - rows)] = 0.0;
       return;
     }
-    // 64 columns x CH rows, 16 B (2 rows) per cp.async; rows past m are zero-filled
+    // 64 columns x CH rows, 16 B (2 rows) per cp.async; rows past m are zero-filled; odd m
+    // leaves every other column 8-byte aligned only -> plain loads
     for (int e = tid; e < KK * CH / 2; e += 256) {
       const int c = e / (CH / 2), r = 2 * (e % (CH / 2));
       double* dst = &stage[buf][c * LDR + r];
-      if (r0 + r + 1 < m) {
+      if (r0 + r + 1 < m && (m & 1) == 0) {
         cpa16(dst, Wb + (size_t)bj_pair_col(c, k, bi, bj) * m + r0 + r);
       } else {
-        dst[0] = r0 + r < m ? Wb[(size_t)bj_pair_col(c, k, bi, bj) * m + r0 + r] : 0.0;
-        dst[1] = 0.0;
+        const double* src = Wb + (size_t)bj_pair_col(c, k, bi, bj) * m + r0 + r;
+        dst[0] = r0 + r < m ? src[0] : 0.0;
+        dst[1] = r0 + r + 1 < m ? src[1] : 0.0;
       }
     }
     cpa_commit();
@@ -366,6 +386,114 @@ __global__ void __launch_bounds__(256) bj_gram_mma(BJGemmArgs<double> a, int ste
     const double e = red;
     bj_atomic_max_pos(a.e_sweep + b, e);
     a.pair_act[slot] = e > a.tol ? 1 : 0;  // pairs at e <= tol are skipped (blockjacobi.py:128-129)
+    bj_count(a.stats, b, e > a.tol);
+  }
+}
+
+// bj_gram_mma fed by 2-D tensor-map TMA (see tma_load_2d): same product, e and mask.
+__global__ void __launch_bounds__(256) bj_gram_tma(BJGemmArgs<double> a, int step, const __grid_constant__ CUtensorMap tmW) {
+  constexpr int KK = kMmaKK, CH = kGramCH, NS = CH / kTmaBoxRows, LDG = KK + 1;
+  constexpr int STAGE = 2 * NS * kTmaBox;  // doubles per buffer (2 blocks x NS boxes)
+  static_assert(2 * STAGE <= KK * LDG, "stages alias G");
+  __shared__ __align__(1024) double sm[KK * LDG + 64];
+  __shared__ double red;
+  __shared__ __align__(8) uint64_t bars[2];
+  double* Gs = sm;
+  const int P = a.nb / 2;
+  const int64_t b = blockIdx.x / P;
+  const int pk = blockIdx.x % P;
+  const int64_t slot = blockIdx.x;
+  if (b >= a.batch) return;
+  if (!a.active[b]) {
+    if (threadIdx.x == 0) a.pair_act[slot] = 0;
+    return;
+  }
+  int bi, bj;
+  rr_pair(a.nb, step, pk, bi, bj);
+  const int k = a.k, m = a.m, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int i0 = (warp >> 1) * 16, j0 = (warp & 1) * 32;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+  }
+  fence_proxy_async();
+  __syncthreads();
+  const int yi = (int)(b * a.n_pad + (int64_t)bi * k), yj = (int)(b * a.n_pad + (int64_t)bj * k);
+  auto load = [&](int buf, int r0) {
+    if (tid == 0) {
+      fence_proxy_async();
+      mbar_expect_tx(&bars[buf], (unsigned)(STAGE * sizeof(double)));
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        tma_load_2d(sm + buf * STAGE + s * kTmaBox, &tmW, &bars[buf], r0 + s * kTmaBoxRows, yi);
+        tma_load_2d(sm + buf * STAGE + (NS + s) * kTmaBox, &tmW, &bars[buf], r0 + s * kTmaBoxRows, yj);
+      }
+    }
+  };
+  double acc[2][4][2];
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  const int nch = (m + CH - 1) / CH;
+  unsigned phase[2] = {0u, 0u};
+  load(0, 0);
+  for (int ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) load((ch + 1) & 1, (ch + 1) * CH);
+    mbar_wait(&bars[ch & 1], phase[ch & 1]);
+    phase[ch & 1] ^= 1u;
+    const double* S = sm + (ch & 1) * STAGE;
+#pragma unroll
+    for (int k0 = 0; k0 < CH; k0 += 4) {
+      const int kr = k0 + t, box = kr / kTmaBoxRows, rr = kr % kTmaBoxRows;
+      double av[2], bv[4];
+#pragma unroll
+      for (int x = 0; x < 2; ++x) {
+        const int i = i0 + 8 * x + g;  // pair column: block i / 32, column i % 32
+        av[x] = S[((i >> 5) * NS + box) * kTmaBox + swz64(i & 31, rr)];
+      }
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        const int j = j0 + 8 * y + g;
+        bv[y] = S[((j >> 5) * NS + box) * kTmaBox + swz64(j & 31, rr)];
+      }
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) dmma_8x8x4(acc[x][y], av[x], bv[y]);
+    }
+    __syncthreads();  // buffer (ch & 1) is reloaded next iteration / aliased by G
+  }
+#pragma unroll
+  for (int x = 0; x < 2; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      Gs[(i0 + 8 * x + g) * LDG + j0 + 8 * y + 2 * t] = acc[x][y][0];
+      Gs[(i0 + 8 * x + g) * LDG + j0 + 8 * y + 2 * t + 1] = acc[x][y][1];
+    }
+  if (tid == 0) red = 0.0;
+  __syncthreads();
+  double* Gout = a.G + slot * KK * KK;
+  double best = 0.0;
+  for (int e = tid; e < KK * KK; e += 256) {
+    const int j = e / KK, i = e % KK;
+    const double gv = i <= j ? Gs[i * LDG + j] : Gs[j * LDG + i];
+    Gout[e] = gv;
+    if (i != j) {
+      const double den = sqrt(fabs(Gs[i * LDG + i])) * sqrt(fabs(Gs[j * LDG + j]));
+      const double num = fabs(gv);
+      const double rt = den > 0.0 ? num / den : (num > 0.0 ? __longlong_as_double(0x7ff0000000000000LL) : 0.0);
+      best = rt > best ? rt : best;
+    }
+  }
+  best = warp_allreduce_max(best);
+  if ((tid & 31) == 0 && best > 0.0) bj_atomic_max_pos(&red, best);
+  __syncthreads();
+  if (tid == 0) {
+    const double e = red;
+    bj_atomic_max_pos(a.e_sweep + b, e);
+    a.pair_act[slot] = e > a.tol ? 1 : 0;
     bj_count(a.stats, b, e > a.tol);
   }
 }
@@ -448,11 +576,11 @@ __global__ void __launch_bounds__(256) bj_rot_mma(BJGemmArgs<double> a, int step
       const int c = e / (CH / 2), r = 2 * (e % (CH / 2));
       double* dst = &X[c * LDX + r];
       const double* src = M + (size_t)bj_pair_col(c, k, bi, bj) * ld + r0 + r;
-      if (r0 + r + 1 < rows) {
+      if (r0 + r + 1 < rows && (ld & 1) == 0) {  // odd ld: 8-byte aligned columns only
         cpa16(dst, src);
       } else {
         dst[0] = r0 + r < rows ? src[0] : 0.0;
-        dst[1] = 0.0;
+        dst[1] = r0 + r + 1 < rows ? src[1] : 0.0;
       }
     }
     cpa_commit();
@@ -503,6 +631,114 @@ __global__ void __launch_bounds__(256) bj_rot_mma(BJGemmArgs<double> a, int step
             const int c = c0w + 8 * y + 2 * t + q;
             // keep exactly-null directions exactly null (blockjacobi.py:133-134)
             const double val = (isw && !(sig[c] != 0.0)) ? 0.0 : acc[x][y][q];
+            M[(size_t)bj_pair_col(c, k, bi, bj) * ld + r] = val;
+          }
+      }
+    }
+    __syncthreads();  // chunk buffer (ch & 1) is reloaded next iteration
+  }
+}
+
+
+// bj_rot_mma fed by 2-D tensor-map TMA: the W and V chunks (64 rows x the pair's 64 columns)
+// arrive as 2 blocks x 8 swizzled 8 x 32 boxes per chunk (block_gemm.cuh tma_load_2d); the
+// A-fragment reads (rows g, column k0 + t) are two wavefronts under the 64B swizzle.
+constexpr int kRotTmaStage = 2 * (kRotCH / kTmaBoxRows) * kTmaBox;  // doubles per chunk buffer
+constexpr size_t kRotTmaSmem = (size_t)(2 * kRotTmaStage + kMmaKK * kRotLDU + kMmaKK) * sizeof(double) + 1024;
+
+__global__ void __launch_bounds__(256) bj_rot_tma(BJGemmArgs<double> a, int step, const __grid_constant__ CUtensorMap tmW,
+                                                  const __grid_constant__ CUtensorMap tmV) {
+  constexpr int KK = kMmaKK, CH = kRotCH, NS = CH / kTmaBoxRows, LDU = kRotLDU, STAGE = kRotTmaStage;
+  extern __shared__ double sm_rot_raw[];
+  double* Xs = (double*)(((uintptr_t)sm_rot_raw + 1023) & ~(uintptr_t)1023);  // swizzle period alignment
+  double* Us = Xs + 2 * STAGE;  // U column-major: U[k][n] at Us[n * LDU + k]
+  double* sig = Us + KK * LDU;
+  __shared__ __align__(8) uint64_t bars[2];
+  const int P = a.nb / 2;
+  const int64_t b = blockIdx.x / P;
+  const int pk = blockIdx.x % P;
+  const int64_t slot = blockIdx.x;
+  if (b >= a.batch || !a.pair_act[slot]) return;
+  int bi, bj;
+  rr_pair(a.nb, step, pk, bi, bj);
+  const int k = a.k, m = a.m, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int r0w = (warp >> 1) * 16, c0w = (warp & 1) * 32;
+  const double* Ug = a.U + slot * KK * KK;
+  for (int e = tid; e < KK * KK / 2; e += 256) {
+    const int c = e / (KK / 2), r = 2 * (e % (KK / 2));
+    cpa16(&Us[c * LDU + r], Ug + (size_t)c * KK + r);
+  }
+  cpa_commit();
+  if (tid < KK) sig[tid] = a.S[slot * KK + tid];
+  double* Wm = a.W + b * (int64_t)m * a.n_pad;
+  double* Vm = a.V ? a.V + b * (int64_t)a.n_pad * a.n_pad : nullptr;
+  const int nw_ch = a.only_v ? 0 : (m + CH - 1) / CH, nv_ch = Vm ? (a.n_pad + CH - 1) / CH : 0;
+  const int nch = nw_ch + nv_ch;
+  if (nch == 0) return;
+  if (tid == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+  }
+  fence_proxy_async();
+  __syncthreads();
+  const int yi = (int)(b * a.n_pad + (int64_t)bi * k), yj = (int)(b * a.n_pad + (int64_t)bj * k);
+  auto load = [&](int buf, int ch) {
+    if (tid == 0) {
+      const bool isw = ch < nw_ch;
+      const CUtensorMap* map = isw ? &tmW : &tmV;
+      const int r0 = (isw ? ch : ch - nw_ch) * CH;
+      double* X = Xs + buf * STAGE;
+      fence_proxy_async();
+      mbar_expect_tx(&bars[buf], (unsigned)(STAGE * sizeof(double)));
+#pragma unroll
+      for (int s = 0; s < NS; ++s) {
+        tma_load_2d(X + s * kTmaBox, map, &bars[buf], r0 + s * kTmaBoxRows, yi);
+        tma_load_2d(X + (NS + s) * kTmaBox, map, &bars[buf], r0 + s * kTmaBoxRows, yj);
+      }
+    }
+  };
+  unsigned phase[2] = {0u, 0u};
+  load(0, 0);
+  cpa_wait<0>();  // U
+  __syncthreads();
+  for (int ch = 0; ch < nch; ++ch) {
+    if (ch + 1 < nch) load((ch + 1) & 1, ch + 1);
+    mbar_wait(&bars[ch & 1], phase[ch & 1]);
+    phase[ch & 1] ^= 1u;
+    const double* X = Xs + (ch & 1) * STAGE;
+    double acc[2][4][2];
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+#pragma unroll 4
+    for (int k0 = 0; k0 < KK; k0 += 4) {
+      const int c = k0 + t;  // pair column: block c / 32, column c % 32
+      double av[2], bv[4];
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+        av[x] = X[((c >> 5) * NS + ((r0w + 8 * x) >> 3)) * kTmaBox + swz64(c & 31, g)];  // A[g][t] = X[r][k]
+#pragma unroll
+      for (int y = 0; y < 4; ++y) bv[y] = Us[(c0w + 8 * y + g) * LDU + k0 + t];  // B[t][g] = U[k][n]
+#pragma unroll
+      for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) dmma_8x8x4(acc[x][y], av[x], bv[y]);
+    }
+    const bool isw = ch < nw_ch;
+    double* M = isw ? Wm : Vm;
+    const int ld = isw ? m : a.n_pad, rows = ld, r0 = (isw ? ch : ch - nw_ch) * CH;
+#pragma unroll
+    for (int x = 0; x < 2; ++x) {
+      const int r = r0 + r0w + 8 * x + g;
+      if (r < rows) {
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int c = c0w + 8 * y + 2 * t + q;
+            const double val = (isw && !(sig[c] != 0.0)) ? 0.0 : acc[x][y][q];  // blockjacobi.py:133-134
             M[(size_t)bj_pair_col(c, k, bi, bj) * ld + r] = val;
           }
       }

@@ -17,6 +17,8 @@
 #include <utility>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "internal.h"
 #include "jacobi_cta.cuh"
 #include "qr_cta.cuh"
@@ -1079,6 +1081,28 @@ static constexpr bool kUseMma(int TT) {
   return sizeof(T) == 8 && TT == 4;
 }
 
+// Tensor map for the 2-D TMA staging of bj_gram_tma: W as a column-major (m rows) x (B n_pad
+// columns) float64 tensor, box 8 x 32, 64-byte swizzle (block_gemm.cuh, tma_load_2d). The encoder
+// is the driver's cuTensorMapEncodeTiled, reached through the runtime (no libcuda link).
+static bool make_col_tmap(CUtensorMap* map, const double* base, int rows, int64_t cols) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }();
+  if (!enc || (rows & 1) || ((uintptr_t)base & 15) || cols > 0x7fffffff) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)rows, (cuuint64_t)cols};
+  const cuuint64_t strides[1] = {(cuuint64_t)rows * sizeof(double)};
+  const cuuint32_t box[2] = {(cuuint32_t)kTmaBoxRows, (cuuint32_t)kTmaBoxCols};
+  const cuuint32_t es[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <typename T>
 static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
   BJArgs<T> a;
@@ -1131,6 +1155,13 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
     return e ? atoi(e) : kBlockTmaDefault;
   }();
   g.tma = tma_sel;
+  // tensor-map TMA kernels (bits 4 / 8); fall back to the cp.async kernels if a map can't be encoded
+  CUtensorMap tm_w{}, tm_v{};
+  int tma_sel_gram = tma_sel & 4, tma_sel_rot = tma_sel & 8;
+  if ((tma_sel & 12) && sizeof(T) == 8 && k == 32) {
+    if (!make_col_tmap(&tm_w, (const double*)a.W, L.m, L.batch * np)) tma_sel_gram = tma_sel_rot = 0;
+    if (a.V && !make_col_tmap(&tm_v, (const double*)a.V, np, L.batch * np)) tma_sel_rot = 0;
+  }
   SvdLaunch in{};
   size_t rot_smem = 0;
   if (bg) {
@@ -1181,6 +1212,7 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
     if (TT == 4) e = smem_optin((const void*)bj_rot<T, 4>, rot_smem);
     if (e == cudaSuccess && kUseMma<T>(TT))
       e = smem_optin((const void*)bj_rot_mma, (size_t)(kRotSmem));
+    if (e == cudaSuccess && kUseMma<T>(TT) && tma_sel_rot) e = smem_optin((const void*)bj_rot_tma, kRotTmaSmem);
     if (e != cudaSuccess) return (int)e;
   }
   // batched direct pipeline (fp64, 2k = 64)
@@ -1241,6 +1273,7 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
     if (e == cudaSuccess)
       e = smem_optin((const void*)bj_dapply_wy, (size_t)(dap_smem));
     if (e == cudaSuccess) e = smem_optin((const void*)bj_rot_mma, (size_t)(kRotSmem));
+    if (e == cudaSuccess && tma_sel_rot) e = smem_optin((const void*)bj_rot_tma, kRotTmaSmem);
     if (e != cudaSuccess) return (int)e;
   }
   // wide pairs (2k > 64): staged pipeline over batched QR / GEMM / SVD launches
@@ -1335,13 +1368,18 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
         int rc = launch_svd(0, in, iws, iws_bytes, st);
         if (rc) return rc;
         bj_dapply_wy<<<grid, 256, dap_smem, st>>>(*reinterpret_cast<BJArgs<double>*>(&a), dd, s);
-        if (a.V) bj_rot_mma<<<grid, 256, kRotSmem, st>>>(*reinterpret_cast<BJGemmArgs<double>*>(&gv), s);
+        if (a.V && tma_sel_rot)
+          bj_rot_tma<<<grid, 256, kRotTmaSmem, st>>>(*reinterpret_cast<BJGemmArgs<double>*>(&gv), s, tm_w, tm_v);
+        else if (a.V)
+          bj_rot_mma<<<grid, 256, kRotSmem, st>>>(*reinterpret_cast<BJGemmArgs<double>*>(&gv), s);
       } else if (bg) {
         const int TT = kk / 16;
         if (TT == 1) bj_gram<T, 1><<<grid, 256, 0, st>>>(g, s);
         if (TT == 2) bj_gram<T, 2><<<grid, 256, 0, st>>>(g, s);
         if (TT == 3) bj_gram<T, 3><<<grid, 256, 0, st>>>(g, s);
-        if (kUseMma<T>(TT))
+        if (kUseMma<T>(TT) && tma_sel_gram)
+          bj_gram_tma<<<grid, 256, 0, st>>>(*reinterpret_cast<BJGemmArgs<double>*>(&g), s, tm_w);
+        else if (kUseMma<T>(TT))
           bj_gram_mma<<<grid, 256, 0, st>>>(*reinterpret_cast<BJGemmArgs<double>*>(&g), s);
         else if (TT == 4)
           bj_gram<T, 4><<<grid, 256, 0, st>>>(g, s);
@@ -1350,7 +1388,9 @@ static int launch_block_t(const BlockLaunch& L, void* ws, cudaStream_t st) {
         if (TT == 1) bj_rot<T, 1><<<grid, 256, rot_smem, st>>>(g, s);
         if (TT == 2) bj_rot<T, 2><<<grid, 256, rot_smem, st>>>(g, s);
         if (TT == 3) bj_rot<T, 3><<<grid, 256, rot_smem, st>>>(g, s);
-        if (kUseMma<T>(TT))
+        if (kUseMma<T>(TT) && tma_sel_rot)
+          bj_rot_tma<<<grid, 256, kRotTmaSmem, st>>>(*reinterpret_cast<BJGemmArgs<double>*>(&g), s, tm_w, tm_v);
+        else if (kUseMma<T>(TT))
           bj_rot_mma<<<grid, 256, kRotSmem, st>>>(*reinterpret_cast<BJGemmArgs<double>*>(&g), s);
         else if (TT == 4)
           bj_rot<T, 4><<<grid, 256, rot_smem, st>>>(g, s);
