@@ -27,12 +27,19 @@ class BatchError(Exception):
 
 def as_matrix(a, dtype=None):
     """Coerce ``a`` to a 2-d column-major float array (core.py:26-33)."""
+    return np.asfortranarray(as_matrix_view(a, dtype))
+
+
+def as_matrix_view(a, dtype=None):
+    """as_matrix's checks and dtype coercion without the Fortran copy: the batched entry points
+    only read their inputs (staged straight into pinned memory by stack_to_device), so the
+    reference's defensive copy (core.py:26-33) would be a second pass over every entry."""
     a = np.asarray(a, dtype=dtype)
     if a.ndim != 2:
         raise ValueError(f"expected a 2-d array, got ndim={a.ndim}")
     if a.dtype.type not in REAL_DTYPES:
         a = a.astype(np.float64)
-    return np.asfortranarray(a)
+    return a
 
 
 def write_matrix_text(path, a):
@@ -117,12 +124,22 @@ def split_contiguous(idx, parts):
     return out
 
 
+PIPELINE_MIN_ENTRIES = 1024  # drop-in groups at least this large use the overlapped host pipeline
+PIPELINE_CHUNKS = 8
+
+
 def run_sharded(mats, idx, devs, launch):
     """One batched call per device over contiguous pieces of ``idx``: every piece is staged and
     launched first (the devices run concurrently; launches are asynchronous), then each piece's
     outputs are brought to the host. launch(store, device, offset) -> dict of device tensors
     (None allowed); offset = the piece's position in ``idx`` (rsvd's global seed index).
-    Returns [(piece, {name: numpy or None})]. Results do not depend on the split (core.py:97-103)."""
+    Returns [(piece, {name: numpy or None})]. Results do not depend on the split (core.py:97-103).
+    One device and a large group: the chunked host pipeline (stream.run_entries_pipelined), which
+    overlaps host staging, both copies and the kernels."""
+    if len(devs) == 1 and len(idx) >= PIPELINE_MIN_ENTRIES:
+        from .stream import run_entries_pipelined
+
+        return [(list(idx), run_entries_pipelined(mats, idx, devs[0], launch, chunks=PIPELINE_CHUNKS))]
     pending = []
     for k, (off, piece) in enumerate(split_contiguous(idx, len(devs))):
         dev = devs[k]
@@ -185,7 +202,7 @@ def group_entries(entries, validate):
     errors = {}
     for i, e in enumerate(entries):
         try:
-            a = as_matrix(e)
+            a = as_matrix_view(e)
             validate(a)
             mats.append(a)
         except Exception as exc:  # noqa: BLE001 - reported with the batch index
@@ -201,13 +218,25 @@ def group_entries(entries, validate):
 
 
 def stack_to_device(mats, idx, device):
-    """Stack entries (Fortran arrays) into pinned host memory, copy to device: (G, n, m)."""
-    first = mats[idx[0]]
-    m, n = first.shape
-    host = torch.empty((len(idx), n, m), dtype=torch_dtype(first.dtype), pin_memory=True)
+    """Stack entries into pinned host memory and copy to the device as column-major storage
+    (G, n, m). Fortran-ordered entries are stacked as they lie (one memcpy each, inside one numpy
+    call); C-ordered ones (numpy's default) are stacked row-major and transposed ON THE DEVICE,
+    so no entry is transposed by the host."""
+    sel = [mats[i] for i in idx]
+    m, n = sel[0].shape
+    dt = torch_dtype(sel[0].dtype)
+    if all(a.flags.f_contiguous for a in sel):
+        host = torch.empty((len(sel), n, m), dtype=dt, pin_memory=True)
+        np.stack([a.T for a in sel], out=host.numpy())
+        return host.to(device, non_blocking=True)
+    if all(a.flags.c_contiguous for a in sel):
+        host = torch.empty((len(sel), m, n), dtype=dt, pin_memory=True)
+        np.stack(sel, out=host.numpy())
+        return host.to(device, non_blocking=True).transpose(1, 2).contiguous()
+    host = torch.empty((len(sel), n, m), dtype=dt, pin_memory=True)
     hv = host.numpy()
-    for j, i in enumerate(idx):
-        hv[j] = mats[i].T
+    for j, a in enumerate(sel):
+        hv[j] = a.T
     return host.to(device, non_blocking=True)
 
 

@@ -168,10 +168,11 @@ def batch_svd(batch, opts=None, *, threads=1, device=None, devices=None):
 
         for piece, h in run_sharded(mats, idx, devs, launch):
             for j, i in enumerate(piece):
+                # per-entry views of the (G, n, m) host arrays: column-major (m, n), no copies
                 out[i] = SvdResult(
-                    u=np.asfortranarray(h["u"][j].T),
-                    sigma=h["s"][j].copy(),
-                    v=None if h["v"] is None else np.asfortranarray(h["v"][j].T),
+                    u=h["u"][j].T,
+                    sigma=h["s"][j],
+                    v=None if h["v"] is None else h["v"][j].T,
                     converged=bool(h["conv"][j]),
                     sweeps=int(h["sweeps"][j]),
                 )

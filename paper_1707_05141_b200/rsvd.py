@@ -15,6 +15,7 @@ import torch
 from . import _lib
 from .core import (
     as_matrix,
+    as_matrix_view,
     check_batched_tensor,
     colmajor,
     from_colmajor,
@@ -154,7 +155,7 @@ def batch_rsvd(batch, opts, *, threads=1, device=None, devices=None):
     mats, errors = [], {}
     for i, e in enumerate(entries):
         try:
-            a = as_matrix(e)
+            a = as_matrix_view(e)
             _check_width(a.shape[0], a.shape[1], opts)
             mats.append(a)
         except Exception as exc:  # noqa: BLE001

@@ -11,9 +11,13 @@ chunking (entries are independent, core.py:97-103), so the output is identical t
 single call.
 """
 
+import os
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
 import torch
 
-from .core import resolve_device
+from .core import resolve_device, torch_dtype
 
 
 def chunk_bounds(B, chunks, taper=True):
@@ -89,3 +93,89 @@ def run_host_pipelined(op, host_in, host_outs, *, chunks=4, device=None, index_b
         main.wait_stream(s_out)
         del keep
     return host_outs
+
+
+_POOL, _POOL_W = None, 1
+
+
+def _stack_chunk(sel, lo, hi, hv, mode):
+    """Host staging of entries [lo, hi) into the pinned buffer, split over a few threads (numpy
+    copies run without the GIL; measured on the B200 hosts: 21.6 ms single-threaded for 5 000
+    64x64 entries, 10.4 ms with 4 threads, slower again with 8)."""
+    global _POOL, _POOL_W
+    if _POOL is None:
+        _POOL_W = max(1, min(4, len(os.sched_getaffinity(0))))
+        _POOL = ThreadPoolExecutor(_POOL_W)
+
+    def part(a, b):
+        if mode == "f":
+            np.stack([x.T for x in sel[a:b]], out=hv[a:b])
+        elif mode == "c":
+            np.stack(sel[a:b], out=hv[a:b])
+        else:
+            for j in range(a, b):
+                hv[j] = sel[j].T
+
+    w = _POOL_W if hi - lo >= 256 else 1
+    step = -(-(hi - lo) // w)
+    list(_POOL.map(lambda a: part(a, min(hi, a + step)), range(lo, hi, step)))
+
+
+def run_entries_pipelined(mats, idx, device, launch, *, chunks=8):
+    """The drop-in path (list of host matrices in, host arrays out) with the same overlap: chunk c
+    is stacked into pinned memory by the host while chunk c-1's copy and kernels run, its H2D,
+    the batched call (launch(store, device, offset) -> dict of device tensors) and its D2H are
+    queued on the pipeline streams, and every output lands in one pinned (B, ...) array.
+    Fortran-ordered entries are stacked as they lie; C-ordered ones row-major and transposed on
+    the device (core.stack_to_device). Returns {name: numpy array or None}."""
+    dev = resolve_device(device)
+    sel = [mats[i] for i in idx]
+    B = len(sel)
+    m, n = sel[0].shape
+    dt = torch_dtype(sel[0].dtype)
+    if all(a.flags.f_contiguous for a in sel):
+        mode = "f"
+    elif all(a.flags.c_contiguous for a in sel):
+        mode = "c"
+    else:
+        mode = "mixed"
+    shape = (B, m, n) if mode == "c" else (B, n, m)
+    host_in = torch.empty(shape, dtype=dt, pin_memory=True)
+    hv = host_in.numpy()
+    outs = {}
+    with torch.cuda.device(dev):
+        s_in, s_out, c0, c1 = _streams(dev)
+        s_comp = [c0, c1]
+        main = torch.cuda.current_stream(dev)
+        for s in (s_in, s_out, *s_comp):
+            s.wait_stream(main)
+        dev_in = torch.empty(shape, dtype=dt, device=dev)
+        keep = []
+        for c, (lo, hi) in enumerate(chunk_bounds(B, chunks, taper=True)):
+            _stack_chunk(sel, lo, hi, hv, mode)
+            ev_in = torch.cuda.Event()
+            with torch.cuda.stream(s_in):
+                dev_in[lo:hi].copy_(host_in[lo:hi], non_blocking=True)
+                ev_in.record(s_in)
+            sc = s_comp[c & 1]
+            sc.wait_event(ev_in)
+            ev_done = torch.cuda.Event()
+            with torch.cuda.stream(sc):
+                x = dev_in[lo:hi]
+                if mode == "c":
+                    x = x.transpose(1, 2).contiguous()
+                res = launch(x, dev, lo)
+                ev_done.record(sc)
+            if not outs:
+                outs = {k: None if v is None else torch.empty((B,) + tuple(v.shape[1:]), dtype=v.dtype, pin_memory=True)
+                        for k, v in res.items()}
+            s_out.wait_event(ev_done)
+            with torch.cuda.stream(s_out):
+                for k, v in res.items():
+                    if v is not None:
+                        outs[k][lo:hi].copy_(v, non_blocking=True)
+            keep.append((x, res))  # device tensors stay alive until their copies have run
+        s_out.synchronize()
+        main.wait_stream(s_out)
+        del keep
+    return {k: None if v is None else v.numpy() for k, v in outs.items()}

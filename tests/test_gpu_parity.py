@@ -651,3 +651,74 @@ def test_rr_log_chunking_is_invisible():
     assert bool(torch.all(r30["converged"])) and int(r30["sweeps"].max()) < 30
     for k in ("u", "sigma", "v", "sweeps", "converged"):
         assert torch.equal(r30[k], r300[k]), k
+
+
+@pytest.mark.parametrize("entry", ["svd", "qr", "block", "rsvd"])
+def test_dropin_input_layouts_identical(entry):
+    """The drop-in batch calls stage C-ordered, Fortran-ordered, strided and mixed entry lists
+    differently (core.stack_to_device: host stack + device transpose / plain stack / per-entry);
+    the results must be bitwise identical, and the inputs untouched (core.py:26-33)."""
+    rng = np.random.default_rng(21)
+    m, n = (96, 64) if entry != "block" else (128, 96)
+    base = [rng.standard_normal((m, n)) for _ in range(6)]
+    layouts = {
+        "c": [np.ascontiguousarray(a) for a in base],
+        "f": [np.asfortranarray(a) for a in base],
+        "strided": [np.repeat(a, 2, axis=1)[:, ::2] for a in base],
+        "mixed": [np.asfortranarray(a) if i % 2 else np.ascontiguousarray(a) for i, a in enumerate(base)],
+    }
+    keep = [a.copy() for a in layouts["c"]]
+
+    def run(batch):
+        if entry == "svd":
+            return [(r.u, r.sigma, r.v) for r in bf.batch_svd(batch, bf.JacobiOptions(accumulate_v=True))]
+        if entry == "qr":
+            return [(r.q, r.r) for r in bf.batch_qr(batch)]
+        if entry == "block":
+            return [(r.u, r.sigma, r.v) for r in
+                    bf.batch_block_svd(batch, bf.BlockJacobiOptions(block_width=16, accumulate_v=True))]
+        return [(r.u, r.s, r.v) for r in bf.batch_rsvd(batch, bf.RsvdOptions(k=8, p=4, seed=3))]
+
+    ref = run(layouts["c"])
+    for name, batch in layouts.items():
+        got = run(batch)
+        for x, y in zip(ref, got):
+            for p, q in zip(x, y):
+                assert np.array_equal(p, q), name
+    for a, b in zip(layouts["c"], keep):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("entry", ["svd", "qr", "rsvd", "block"])
+@pytest.mark.parametrize("order", ["c", "f"])
+def test_dropin_pipelined_matches_tensor_api(entry, order):
+    """Large drop-in groups run the chunked host pipeline (stream.run_entries_pipelined: host
+    staging, H2D, kernels and D2H overlapped); results bitwise equal to one tensor-API call."""
+    B, m, n = (1100, 64, 48) if entry != "block" else (1030, 72, 64)
+    a = dev_gauss(B, m, n, 7_700_000 + m)
+    host = a.cpu().numpy()
+    ents = [np.ascontiguousarray(x) if order == "c" else np.asfortranarray(x) for x in host]
+    if entry == "svd":
+        opts = bf.JacobiOptions(ordering="round_robin", accumulate_v=True)
+        got = bf.batch_svd(ents, opts)
+        r = bf.svd_tensor(a, opts)
+        pairs = [("u", "u"), ("sigma", "sigma"), ("v", "v")]
+    elif entry == "qr":
+        got = bf.batch_qr(ents)
+        q, rr = bf.qr_tensor(a)
+        r = {"q": q, "r": rr}
+        pairs = [("q", "q"), ("r", "r")]
+    elif entry == "block":
+        opts = bf.BlockJacobiOptions(block_width=16, accumulate_v=True, max_sweeps=4)
+        got = bf.batch_block_svd(ents, opts)
+        r = bf.block_svd_tensor(a, opts)
+        pairs = [("u", "u"), ("sigma", "sigma"), ("v", "v")]
+    else:
+        opts = bf.RsvdOptions(k=8, p=4, seed=11)
+        got = bf.batch_rsvd(ents, opts)
+        r = bf.rsvd_tensor(a, opts)
+        pairs = [("u", "u"), ("s", "s"), ("v", "v")]
+    for attr, key in pairs:
+        ref = r[key].cpu().numpy()
+        for i in (0, 1, B // 2, B - 1):
+            assert np.array_equal(getattr(got[i], attr), ref[i]), (attr, i)
