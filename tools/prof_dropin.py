@@ -1,3 +1,8 @@
+"""Profile the drop-in list call (batch_svd on 5 000 host 64x64 matrices, cfg3): wall time of one
+call and the cProfile hot spots (host staging, result construction, synchronisation).
+
+    PYTHONPATH=. python tools/prof_dropin.py
+"""
 import time, numpy as np, torch, cProfile, pstats, io
 import paper_1707_05141_b200 as bf
 a = bf.gaussian_tensor(5000, 64, 64, 3_000_000, seed_mode="add")
