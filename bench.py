@@ -225,10 +225,10 @@ class GpuConfig:
     def kernel_name(self):
         c = self.cfg
         if c["kind"] == "svd":
-            return "svd_rr_kernel + svd_rr_vkernel" if c["ordering"] == "round_robin" else "svd_reg_kernel"
+            return "svd_rr_kernel + svd_rr_vcol_kernel" if c["ordering"] == "round_robin" else "svd_reg_kernel"
         if c["kind"] == "block" and c.get("method", "gram") == "direct":
-            return "bj_dqr_reg + svd_rr_kernel + svd_rr_vkernel (inner) + bj_dapply_wy + bj_rot_mma"
-        return {"qr": "qr_reg_kernel", "block": "bj_gram_mma + svd_rr_kernel (inner) + bj_rot_mma",
+            return "bj_dqr_reg + svd_rr_kernel + svd_rr_vcol_kernel (inner) + bj_dapply_wy + bj_rot_tma"
+        return {"qr": "qr_reg_kernel", "block": "bj_gram_tma + svd_rr_kernel (inner) + bj_rot_tma",
                 "rsvd": "gemm_mma_kernel + qr_reg_kernel + svd_rr_kernel + svd_rr_vkernel"}[c["kind"]]
 
     def work(self):

@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(256) bj_gram_mma(BJGemmArgs<double> a, int ste
   // even m: every column segment starts 16-byte aligned -> TMA bulk copies (warp 0 issues one
   // per column); odd m: 16-byte cp.async per 2 rows
   const bool tma = (a.tma & 1) && (m & 1) == 0;
-  unsigned phase[2] = {0u, 0u};
+  unsigned phase = 0u;  // bit b: parity of buffer b's next completion (a register, not a local array)
   if (tma) {
     if (tid == 0) {
       mbar_init(&bars[0], 1);
@@ -333,8 +333,8 @@ __global__ void __launch_bounds__(256) bj_gram_mma(BJGemmArgs<double> a, int ste
   for (int ch = 0; ch < nch; ++ch) {
     if (ch + 1 < nch) load((ch + 1) & 1, (ch + 1) * CH);
     if (tma) {
-      mbar_wait(&bars[ch & 1], phase[ch & 1]);
-      phase[ch & 1] ^= 1u;
+      mbar_wait(&bars[ch & 1], (phase >> (ch & 1)) & 1u);
+      phase ^= 1u << (ch & 1);
     } else if (ch + 1 < nch) {
       cpa_wait<1>();
     } else {
@@ -437,12 +437,12 @@ __global__ void __launch_bounds__(256) bj_gram_tma(BJGemmArgs<double> a, int ste
 #pragma unroll
     for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
   const int nch = (m + CH - 1) / CH;
-  unsigned phase[2] = {0u, 0u};
+  unsigned phase = 0u;  // bit b: parity of buffer b's next completion (a register, not a local array)
   load(0, 0);
   for (int ch = 0; ch < nch; ++ch) {
     if (ch + 1 < nch) load((ch + 1) & 1, (ch + 1) * CH);
-    mbar_wait(&bars[ch & 1], phase[ch & 1]);
-    phase[ch & 1] ^= 1u;
+    mbar_wait(&bars[ch & 1], (phase >> (ch & 1)) & 1u);
+    phase ^= 1u << (ch & 1);
     const double* S = sm + (ch & 1) * STAGE;
 #pragma unroll
     for (int k0 = 0; k0 < CH; k0 += 4) {
@@ -543,7 +543,7 @@ __global__ void __launch_bounds__(256) bj_rot_mma(BJGemmArgs<double> a, int step
   };
   // even leading dimensions: TMA bulk copies, one per column segment, issued by warp 0
   const bool tma = (a.tma & 2) && (m & 1) == 0 && (a.n_pad & 1) == 0;
-  unsigned phase[2] = {0u, 0u};
+  unsigned phase = 0u;  // bit b: parity of buffer b's next completion (a register, not a local array)
   if (tma) {
     if (tid == 0) {
       mbar_init(&bars[0], 1);
@@ -590,8 +590,8 @@ __global__ void __launch_bounds__(256) bj_rot_mma(BJGemmArgs<double> a, int step
     if (ch + 1 < nch) load((ch + 1) & 1, ch + 1);
     if (tma) {
       if (ch == 0) cpa_wait<0>();  // U (cp.async)
-      mbar_wait(&bars[ch & 1], phase[ch & 1]);
-      phase[ch & 1] ^= 1u;
+      mbar_wait(&bars[ch & 1], (phase >> (ch & 1)) & 1u);
+      phase ^= 1u << (ch & 1);
     } else if (ch + 1 < nch) {
       cpa_wait<1>();
     } else {
@@ -698,14 +698,14 @@ __global__ void __launch_bounds__(256) bj_rot_tma(BJGemmArgs<double> a, int step
       }
     }
   };
-  unsigned phase[2] = {0u, 0u};
+  unsigned phase = 0u;  // bit b: parity of buffer b's next completion (a register, not a local array)
   load(0, 0);
   cpa_wait<0>();  // U
   __syncthreads();
   for (int ch = 0; ch < nch; ++ch) {
     if (ch + 1 < nch) load((ch + 1) & 1, ch + 1);
-    mbar_wait(&bars[ch & 1], phase[ch & 1]);
-    phase[ch & 1] ^= 1u;
+    mbar_wait(&bars[ch & 1], (phase >> (ch & 1)) & 1u);
+    phase ^= 1u << (ch & 1);
     const double* X = Xs + (ch & 1) * STAGE;
     double acc[2][4][2];
 #pragma unroll

@@ -46,8 +46,8 @@ CONFIG_OF = {"cfg1_svd_reg": "cfg1", "cfg2_qr_reg": "cfg2", "cfg3_svd_reg": "cfg
 
 # configs whose hot path is several kernels per step: the captured launches are summed
 CONFIG_SUM = {"cfg3": ["cfg3_svd_rr", "cfg3_svd_rr_v"],  # sweep kernel + V replay (svd_rr_vcol_kernel)
-              "cfg4": ["cfg4_bj_gram_mma", "cfg4_svd_rr_inner", "cfg4_bj_rot_mma"],
-              "cfg4d": ["cfg4d_bj_dqr_reg", "cfg4d_bj_dapply_wy"]}
+              "cfg4": ["cfg4_bj_gram_tma", "cfg4_svd_rr_inner", "cfg4_bj_rot_tma"],
+              "cfg4d": ["cfg4d_bj_dqr_reg", "cfg4d_bj_dapply_wy", "cfg4d_bj_rot_tma"]}
 
 
 def num(x):

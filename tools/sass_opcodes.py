@@ -50,7 +50,7 @@ def main(src):
         cells = " | ".join(f"{c[x] / 1e6:.2f}" if c[x] else "0" for x in CLASSES)
         print(f"| {f[:-11]} | `{k}` | {c['_total'] / 1e6:.1f} | {cells} |")
     print("\n(millions of warp-level instructions executed in the captured launch; DMMA = FP64 tensor-core "
-          "mma.sync.m8n8k4, LDGSTS = cp.async global->shared, UBLKCP = cp.async.bulk (TMA engine))")
+          "mma.sync.m8n8k4, LDGSTS = cp.async global->shared, UBLKCP = cp.async.bulk (1-D TMA), UTMALDG = cp.async.bulk.tensor (2-D tensor-map TMA), SYNCS = mbarrier ops)")
 
 
 if __name__ == "__main__":
