@@ -136,3 +136,50 @@ def test_f32_promotion_engaged(monkeypatch):
     monkeypatch.setenv("BF_F32_NATIVE", "1")
     native = L.bf_svd_workspace_size(1000, 64, 64, 4, ctypes.byref(opts))
     assert promoted >= 2 * 1000 * 64 * 64 * 8 > native
+
+
+def _edge_batch(m, n, rng):
+    a = rng.standard_normal((4, m, n)).astype(np.float32)
+    a[0] = 0.0                       # zero matrix: sigma 0, U completed (jacobi.py:189-209)
+    a[1][:, 3] = 0.0                 # one zero column
+    a[2][:, 5] = a[2][:, 1]          # duplicate columns (rank deficient)
+    a[3][:, :] *= np.float32(1e-6)   # small scale (squared dot products still normal in float32)
+    return a
+
+
+@pytest.mark.parametrize("m,n,ordering", [(32, 32, "serial"), (32, 32, "round_robin"), (64, 64, "round_robin")])
+def test_svd_f32_edge_cases(mode, m, n, ordering):
+    a = _edge_batch(m, n, np.random.default_rng(3))
+    r = bf.svd_tensor(torch.as_tensor(a).cuda(), bf.JacobiOptions(ordering=ordering, accumulate_v=True))
+    o = orc.batch_svd_stacked(np.ascontiguousarray(a.transpose(0, 2, 1)), m, n, ordering=ordering, accumulate_v=True,
+                              threads=4)
+    s, cv = r["sigma"].cpu().numpy(), r["converged"].cpu().numpy()
+    u = r["u"].cpu().numpy().astype(np.float64)
+    for b in range(4):
+        assert bool(cv[b]) == bool(o["converged"][b])
+        if o["s"][b][0] > 0:
+            assert sigma_normwise(s[b], o["s"][b]) <= 1e-5
+        else:
+            assert np.all(s[b] == 0)
+        # U stays orthonormal, zero directions completed
+        assert np.abs(u[b].T @ u[b] - np.eye(n)).max() < 1e-4
+
+
+@pytest.mark.parametrize("m,n", [(64, 32), (128, 40)])
+def test_qr_f32_edge_cases(mode, m, n):
+    a = _edge_batch(m, n, np.random.default_rng(4))
+    q, rr = bf.qr_tensor(torch.as_tensor(a).cuda())
+    qo, ro, bad = orc.batch_qr_stacked(np.ascontiguousarray(a.transpose(0, 2, 1)), m, n, 16, threads=4)
+    eps = np.finfo(np.float32).eps
+    qg, rg = q.cpu().numpy().astype(np.float64), rr.cpu().numpy().astype(np.float64)
+    for b in range(4):
+        scale = float(np.linalg.norm(a[b].astype(np.float64)))
+        # orthonormal Q, QR = A, exact zeros below the diagonal: every entry
+        assert np.abs(qg[b].T @ qg[b] - np.eye(n)).max() < 1e-5
+        assert np.abs(qg[b] @ rg[b] - a[b]).max() <= 64 * eps * max(scale, np.finfo(np.float32).tiny)
+        assert np.all(np.tril(rg[b], -1) == 0)
+        # elementwise against the oracle where the factorisation is unique (full column rank; the
+        # duplicate-column entry's trailing reflectors are built from rounding noise)
+        if b != 2:
+            assert np.abs(qg[b] - qo[b].T).max() <= 64 * eps * max(scale, 1.0)
+            assert np.abs(rg[b] - ro[b].T).max() <= 64 * eps * max(scale, 1.0)
