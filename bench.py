@@ -512,7 +512,7 @@ def measure(name, cfg, device, rank, world, args, flush, peaks, barrier, max_ove
 # per-config e2e pipeline chunks (default; --e2e-chunks overrides). Measured per config: the
 # PCIe-bound cfg2/cfg3/cfg5 overlap best with many chunks; cfg1 (latency-bound) with 2; the
 # wave-bound block configs unchunked (cfg4 4 321 vs 3 911 matrices/s at 2 chunks, cfg4d 2 215 vs 2 155)
-E2E_CHUNKS = {"cfg1": 2, "cfg2": 12, "cfg3": 12, "cfg4": 1, "cfg4d": 1, "cfg5": 8}
+E2E_CHUNKS = {"cfg1": 2, "cfg2": 12, "cfg3": 12, "cfg4": 1, "cfg4d": 1, "cfg5": 12}
 
 BATCH_SWEEP = [125, 250, 500, 1000, 2000, 4000, 8000, 16000]
 
