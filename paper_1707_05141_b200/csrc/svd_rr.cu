@@ -717,7 +717,11 @@ struct VColCfg {
   static constexpr int NPAIR = NP / 2, L = NP - 1;
   static constexpr int THREADS = ((NP + 31) / 32) * 32;
   static constexpr int pick(int d) { return d < 6 ? (L * NPAIR * 16 <= 20 * 1024 ? L : 1) : (L % d == 0 ? d : pick(d - 1)); }
+#ifdef BF_VCOL_VST
+  static constexpr int VST = (L % BF_VCOL_VST == 0) ? BF_VCOL_VST : pick(16);  // A/B override
+#else
   static constexpr int VST = pick(16);  // steps per coefficient stage
+#endif
   static constexpr int STAGES = L / VST;
 };
 
