@@ -397,6 +397,14 @@ BF_DEV typename Zig<T>::U shfl_draw(typename Zig<T>::U v, int src) {
   return __shfl_sync(FULL, v, src);
 }
 
+// maps {0,1} -> {0,1} as 2-bit codes (bit s = f(s)); fn_comp(g, f) = g o f
+constexpr int kFnZero = 0, kFnNot = 1, kFnId = 2, kFnOne = 3;
+BF_DEV int fn_comp(int g, int f) { return ((g >> (f & 1)) & 1) | (((g >> ((f >> 1) & 1)) & 1) << 1); }
+
+#ifndef BF_GAUSS_SERIAL_SLOW
+#define BF_GAUSS_SERIAL_SLOW 0
+#endif
+
 template <typename T>
 __global__ void gaussian_kernel(int64_t batch, int rows, int cols, uint64_t seed_lo, uint64_t seed_hi,
                                 int64_t index_base, int seed_mode, uint64_t xor_mask, T* out, int64_t out_stride,
@@ -434,9 +442,9 @@ __global__ void gaussian_kernel(int64_t batch, int rows, int cols, uint64_t seed
     bool fast[D];
 #pragma unroll
     for (int q = 0; q < D; ++q) fast[q] = Z::fast(d[q], x[q]);
-    // the batch is consumed from `pos` on; every slow-path event is resolved inside it (its
-    // extra draws come from the batch's registers when they lie in it), so Philox runs once
-    // per 32 D draws instead of once per event
+#if BF_GAUSS_SERIAL_SLOW
+    // (previous design, kept for A/B) the batch is consumed from `pos` on; every slow-path event
+    // is resolved inside it by lane 0 while the warp waits, splitting the batch at each event
     while (k < total && pos < bend) {
       const uint64_t lane0 = (blk + lane) * D;  // stream position of this lane's draw 0
       int rej = D;
@@ -492,6 +500,99 @@ __global__ void gaussian_kernel(int64_t batch, int rows, int cols, uint64_t seed
       k += produced;
       pos = p;
     }
+#else
+    // One pass per batch. Which positions start a draw is a linear recurrence -- position P
+    // starts a draw unless P - 1 started one that failed the fast test (its wedge test consumes
+    // P as the uniform) -- so each position's transition start[P-1] -> start[P] is one of
+    // {const 0 (before pos), const 1, NOT}; composing them is a warp scan. Every wedge test of
+    // the batch then runs in parallel on its own lane, and one more scan packs the accepted
+    // draws in stream order. Only a tail event (idx 0, an unbounded number of words) ends the
+    // batch early and is resolved by lane 0.
+    const uint64_t P0 = (blk + lane) * D;  // stream position of this lane's draw 0
+    bool rej[D];
+#pragma unroll
+    for (int q = 0; q < D; ++q) rej[q] = !fast[q];
+    const bool prev_rej = __shfl_up_sync(FULL, (int)rej[D - 1], 1) != 0;
+    int tr[D], F = kFnId;
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      const uint64_t P = P0 + q;
+      tr[q] = P < pos ? kFnZero : (P == pos ? kFnOne : ((q == 0 ? prev_rej : rej[q - 1]) ? kFnNot : kFnOne));
+      F = fn_comp(tr[q], F);
+    }
+    int h = F;
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      const int y = __shfl_up_sync(FULL, h, dd);
+      if (lane >= dd) h = fn_comp(h, y);
+    }
+    int S = __shfl_up_sync(FULL, h, 1);
+    int sv = lane == 0 ? 0 : (S & 1);  // start[P0 - 1]
+    bool st[D];
+    int qt = D;  // first draw of this lane that starts a tail event
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      sv = (tr[q] >> sv) & 1;
+      st[q] = sv != 0;
+      if (st[q] && rej[q] && (d[q] & 0xff) == 0 && qt == D) qt = q;
+    }
+    const unsigned tball = __ballot_sync(FULL, qt < D);
+    const int Lt = tball ? __ffs(tball) - 1 : 32;
+    const int qlim = lane < Lt ? D : (lane == Lt ? qt : 0);  // this lane's draws before the tail
+    const U nxt0 = shfl_draw<T>(d[0], lane < 31 ? lane + 1 : lane);
+    T val[D];
+    bool prod[D];
+    int cnt = 0;
+#pragma unroll
+    for (int q = 0; q < D; ++q) {
+      prod[q] = false;
+      val[q] = x[q];
+      if (q < qlim && st[q]) {
+        if (fast[q]) {
+          prod[q] = true;
+        } else {  // wedge test with the next position's word as the uniform
+          uint64_t p = P0 + q + 1;
+          const U nx = q + 1 < D ? d[(q + 1) % D] : nxt0;
+          T v;
+          if (Z::slow(d[q], nx, q + 1 < D || lane < 31, k0, k1, p, v)) {
+            prod[q] = true;
+            val[q] = v;
+          }
+        }
+      }
+      cnt += prod[q] ? 1 : 0;
+    }
+    int incl = cnt;
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, dd);
+      if (lane >= dd) incl += y;
+    }
+    int off = incl - cnt;
+#pragma unroll
+    for (int q = 0; q < D; ++q)
+      if (prod[q]) store(k + off++, val[q]);
+    k += __shfl_sync(FULL, incl, 31);
+    if (Lt < 32) {  // tail event at lane Lt, draw qt: lane 0 runs it, the next batch starts after it
+      U r_t = d[0];
+      const int q_t = __shfl_sync(FULL, qt, Lt);
+#pragma unroll
+      for (int q = 1; q < D; ++q) r_t = q == q_t ? d[q] : r_t;
+      r_t = shfl_draw<T>(r_t, Lt);
+      uint64_t p = (blk + Lt) * D + q_t + 1;
+      if (lane == 0 && k < total) {
+        T v;
+        if (Z::slow(r_t, r_t, false, k0, k1, p, v)) store(k, v);
+      }
+      p = __shfl_sync(FULL, p, 0);
+      k += 1;
+      pos = p;
+    } else {
+      // a wedge event on the batch's last position consumed the next batch's first word
+      const bool last = __shfl_sync(FULL, (int)(st[D - 1] && rej[D - 1]), 31) != 0;
+      pos = bend + (last ? 1 : 0);
+    }
+#endif
   }
 }
 
