@@ -404,6 +404,9 @@ BF_DEV int fn_comp(int g, int f) { return ((g >> (f & 1)) & 1) | (((g >> ((f >> 
 #ifndef BF_GAUSS_SERIAL_SLOW
 #define BF_GAUSS_SERIAL_SLOW 0
 #endif
+#ifndef BF_GAUSS_NB
+#define BF_GAUSS_NB 1
+#endif
 
 template <typename T>
 __global__ void gaussian_kernel(int64_t batch, int rows, int cols, uint64_t seed_lo, uint64_t seed_hi,
@@ -411,7 +414,8 @@ __global__ void gaussian_kernel(int64_t batch, int rows, int cols, uint64_t seed
                                 int c_order) {
   using Z = Zig<T>;
   using U = typename Z::U;
-  constexpr int D = Z::D;
+  constexpr int NB = BF_GAUSS_NB;  // Philox blocks per lane per batch
+  constexpr int D = Z::D * NB;     // draws per lane per batch
   const int lane = threadIdx.x & 31;
   const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (b >= batch) return;
@@ -434,10 +438,16 @@ __global__ void gaussian_kernel(int64_t batch, int rows, int cols, uint64_t seed
     // one batch: lane l holds draws D (blk + l) .. D (blk + l) + D - 1
     const uint64_t blk = pos / D;
     const uint64_t bend = (blk + 32) * D;
-    uint64_t w[4];
-    philox_block(k0, k1, blk + lane, w);
     U d[D];
-    Z::split(w, d);
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+      uint64_t w[4];
+      philox_block(k0, k1, (blk + lane) * NB + nb, w);
+      U dd[Z::D];
+      Z::split(w, dd);
+#pragma unroll
+      for (int q = 0; q < Z::D; ++q) d[nb * Z::D + q] = dd[q];
+    }
     T x[D];
     bool fast[D];
 #pragma unroll
