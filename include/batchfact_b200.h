@@ -7,7 +7,7 @@
  *   bf_svd_batched_*        replaces batch_svd       jacobi.py:287-290   (per entry: svd, jacobi.py:231-284)
  *   bf_block_svd_batched_*  replaces batch_block_svd blockjacobi.py:171-174 (block_svd, :84-168)
  *   bf_rsvd_batched_*       replaces batch_rsvd      rsvd.py:79-86       (rsvd, rsvd.py:56-76)
- *   bf_gaussian_batched_f64 replaces gaussian_matrix rsvd.py:42-53 (numpy Philox4x64 + ziggurat, bitwise)
+ *   bf_gaussian_batched_*   replaces gaussian_matrix rsvd.py:42-53 (numpy Philox4x64 + ziggurat, bitwise)
  *
  * Conventions (all of them the reference's):
  *   - every matrix is column-major with ld = rows; a batch is `batch` equally shaped
@@ -17,7 +17,11 @@
  *     k + p <= min(m, n) for rsvd (rsvd.py:60-64): violations return BF_ERR_ARG before any
  *     launch, with the reference's message in bf_last_error();
  *   - non-convergence is never an error: per-entry `converged` flags and `sweeps` counts;
- *   - workspace: query bf_*_workspace_size() and pass at least that many device bytes.
+ *   - workspace: query bf_*_workspace_size() and pass at least that many device bytes;
+ *   - the _f32 entry points keep float32 in / out and float32 semantics (default tolerances,
+ *     numpy's float32 Gaussian stream) and compute on the float64 tiers where those cover the
+ *     shape (QR, rr / register SVD, block direct, rsvd); their workspace query (es = 4)
+ *     includes the widened copies. BF_F32_NATIVE=1 in the environment keeps float32 arithmetic.
  *
  * Return: BF_OK (0) or a negative BF_ERR_* code (or a positive cudaError_t value).
  */
