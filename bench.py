@@ -490,7 +490,7 @@ def measure(name, cfg, device, rank, world, args, flush, peaks, barrier, max_ove
         # host-buffer pipeline depth: enough chunks to overlap the PCIe copies with compute, but each
         # chunk must stay a full-GPU call (the small and block configs are latency / wave bound:
         # 12 chunks of cfg1 or cfg4 would each run at one matrix's latency)
-        chunks = args.e2e_chunks if args.e2e_chunks != 0 else -E2E_CHUNKS.get(name, 12)
+        chunks = args.e2e_chunks if args.e2e_chunks != 0 else E2E_CHUNKS.get(name, -12)
         t_e2e, h2d, d2h = time_e2e(gc, e2e_steps, chunks)
         t_e2e = max_over_ranks(t_e2e)
         ent["e2e"] = {"value": gc.global_batch * e2e_steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d,
@@ -509,10 +509,13 @@ def measure(name, cfg, device, rank, world, args, flush, peaks, barrier, max_ove
     return ent
 
 
-# per-config e2e pipeline chunks (default; --e2e-chunks overrides). Measured per config: the
-# PCIe-bound cfg2/cfg3/cfg5 overlap best with many chunks; cfg1 (latency-bound) with 2; the
-# wave-bound block configs unchunked (cfg4 4 321 vs 3 911 matrices/s at 2 chunks, cfg4d 2 215 vs 2 155)
-E2E_CHUNKS = {"cfg1": 2, "cfg2": 12, "cfg3": 12, "cfg4": 1, "cfg4d": 1, "cfg5": 12}
+# per-config e2e pipeline chunks (default; --e2e-chunks overrides; positive = first and last chunk
+# half-sized, negative = equal chunks). Measured per config: the PCIe-bound cfg2/cfg3/cfg5 overlap
+# best with ~10 tapered chunks -- cfg3 at 10 keeps every full chunk (556 matrices) within one wave
+# of the persistent 592-CTA kernel: 589 k vs 556 k matrices/s untapered at 12, 539 k at 9, 562 k at
+# 11; cfg1 (latency-bound) with 2; the wave-bound block configs unchunked (cfg4 4 321 vs 3 911
+# matrices/s at 2 chunks, cfg4d 2 215 vs 2 155)
+E2E_CHUNKS = {"cfg1": -2, "cfg2": 10, "cfg3": 10, "cfg4": -1, "cfg4d": -1, "cfg5": 12}
 
 BATCH_SWEEP = [125, 250, 500, 1000, 2000, 4000, 8000, 16000]
 
