@@ -41,13 +41,16 @@ def chunk_bounds(B, chunks, taper=True):
 _STREAMS = {}
 
 
+COMPUTE_STREAMS = int(os.environ.get("BF_PIPE_COMPUTE_STREAMS", "2"))
+
+
 def _streams(dev):
-    """One set of pipeline streams per device, reused across calls so the caching allocator can
-    recycle the per-stream blocks of earlier calls (fresh streams would force new cudaMallocs)."""
+    """One set of pipeline streams per device (copy-in, copy-out, COMPUTE_STREAMS compute streams
+    the chunks rotate over), reused across calls so the caching allocator can recycle the
+    per-stream blocks of earlier calls (fresh streams would force new cudaMallocs)."""
     key = dev.index
     if key not in _STREAMS:
-        _STREAMS[key] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev), torch.cuda.Stream(dev),
-                         torch.cuda.Stream(dev))
+        _STREAMS[key] = tuple(torch.cuda.Stream(dev) for _ in range(2 + COMPUTE_STREAMS))
     return _STREAMS[key]
 
 
@@ -66,8 +69,7 @@ def run_host_pipelined(op, host_in, host_outs, *, chunks=4, device=None, index_b
         return host_outs
     bounds = chunk_bounds(B, chunks, taper)
     with torch.cuda.device(dev):
-        s_in, s_out, c0, c1 = _streams(dev)
-        s_comp = [c0, c1]
+        s_in, s_out, *s_comp = _streams(dev)
         main = torch.cuda.current_stream(dev)
         for s in (s_in, s_out, *s_comp):
             s.wait_stream(main)
@@ -78,7 +80,7 @@ def run_host_pipelined(op, host_in, host_outs, *, chunks=4, device=None, index_b
             with torch.cuda.stream(s_in):
                 dev_in[lo:hi].copy_(host_in[lo:hi], non_blocking=True)
                 ev_in.record(s_in)
-            sc = s_comp[c & 1]
+            sc = s_comp[c % len(s_comp)]
             sc.wait_event(ev_in)
             ev_done = torch.cuda.Event()
             with torch.cuda.stream(sc):
@@ -144,8 +146,7 @@ def run_entries_pipelined(mats, idx, device, launch, *, chunks=8):
     hv = host_in.numpy()
     outs = {}
     with torch.cuda.device(dev):
-        s_in, s_out, c0, c1 = _streams(dev)
-        s_comp = [c0, c1]
+        s_in, s_out, *s_comp = _streams(dev)
         main = torch.cuda.current_stream(dev)
         for s in (s_in, s_out, *s_comp):
             s.wait_stream(main)
@@ -157,7 +158,7 @@ def run_entries_pipelined(mats, idx, device, launch, *, chunks=8):
             with torch.cuda.stream(s_in):
                 dev_in[lo:hi].copy_(host_in[lo:hi], non_blocking=True)
                 ev_in.record(s_in)
-            sc = s_comp[c & 1]
+            sc = s_comp[c % len(s_comp)]
             sc.wait_event(ev_in)
             ev_done = torch.cuda.Event()
             with torch.cuda.stream(sc):
